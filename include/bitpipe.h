@@ -1,0 +1,152 @@
+/*
+ * bitpipe.h -- C ABI of libbitpipe_b200.so, the sm_100a compute library of
+ * the B200-native BitPipe train step.
+ *
+ * The reference (pipesched, pure Python) has NO native interface: its
+ * train step exists only as the SPEC's `run_schedule_numeric(schedule,
+ * model, batch, seed)` (reference SPEC.md:426-434) and its per-task
+ * semantics ("each worker executes its task list in order;
+ * activations/gradients flow along schedule edges; gradients accumulate
+ * over micro-batches; ... replica gradients are averaged (allreduce) before
+ * the single weight update").  Each entry point below is one piece of that
+ * per-task work; INTEGRATION.md maps them onto the reference's call sites
+ * and shows the ctypes binding the Python host driver uses.
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers owned by the caller (the library
+ *     never allocates or frees caller memory).  `stream` is a cudaStream_t
+ *     passed as void*.  Every call is asynchronous on that stream.
+ *   - Matrices are row-major with an explicit leading dimension in
+ *     ELEMENTS.  Token-major activations are [rows = B*S, cols = hidden].
+ *   - Return value: BP_OK (0) or an error code; bp_last_error() gives a
+ *     thread-local message.  Errors are never swallowed and there is no
+ *     CPU fallback: a missing GPU or unsupported shape is an error.
+ */
+#ifndef BITPIPE_B200_H
+#define BITPIPE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BP_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define BP_API __attribute__((visibility("default")))
+#else
+#define BP_API
+#endif
+
+enum bp_status { BP_OK = 0, BP_ERR_INVALID = 1, BP_ERR_CUDA = 2, BP_ERR_UNSUPPORTED = 3 };
+enum bp_dtype { BP_F32 = 0, BP_BF16 = 1 };
+enum bp_epilogue {
+  BP_EPI_NONE = 0,  /* C = alpha*acc (+bias) (+residual) (+C if beta) */
+  BP_EPI_GELU = 1,  /* aux = alpha*acc + bias ; C = gelu(aux)            */
+  BP_EPI_DGELU = 2  /* C = alpha*acc * gelu'(aux)   (aux = saved pre-act)  */
+};
+
+/* ---------------------------------------------------------------- misc -- */
+BP_API int bp_abi_version(void);
+BP_API const char* bp_last_error(void);
+/* Number of SMs of `device` (sizing persistent grids); <0 on error. */
+BP_API int bp_sm_count(int device);
+/* 1 if the tcgen05 GEMM path is usable on the current device. */
+BP_API int bp_tc_available(void);
+/* Count of kernels this library launched since load (per process). */
+BP_API unsigned long long bp_launch_count(void);
+/* Process-wide switches (testing aids): route attention to the exact
+ * kernel / GEMMs to the SIMT kernel even when the fast path applies. */
+enum bp_option { BP_OPT_ATTN_EXACT = 1, BP_OPT_GEMM_SIMT = 2 };
+BP_API int bp_set_option(int option, int value);
+
+/* ---------------------------------------------------------------- GEMM --
+ * C[M,N] = epilogue( alpha * op(A)[M,K] . op(B)[K,N] )
+ *   a_kmajor = 1 : A stored [M,K] (row-major, lda >= K)
+ *   a_kmajor = 0 : A stored [K,M] (row-major, lda >= M)
+ *   b_kmajor = 1 : B stored [N,K] (row-major, ldb >= K)   ("x W^T")
+ *   b_kmajor = 0 : B stored [K,N] (row-major, ldb >= N)
+ * in_dtype BP_BF16 runs the tcgen05/TMEM/TMA tensor-core kernel (fp32
+ * accumulate); BP_F32 runs an exact-fp32 SIMT kernel (check mode, no TF32).
+ * beta must be 0 or 1; beta = 1 accumulates into C (C must be fp32).
+ * bias: [N] in in_dtype or NULL.  residual: [M,N] in c_dtype or NULL.
+ * aux : [M,N] in c_dtype (GELU pre-activation) for BP_EPI_GELU/DGELU.
+ */
+typedef struct bp_gemm_args {
+  int M, N, K;
+  int in_dtype;
+  int a_kmajor, b_kmajor;
+  const void* A; int64_t lda;
+  const void* B; int64_t ldb;
+  void* C; int64_t ldc; int c_dtype;
+  float alpha, beta;
+  const void* bias;
+  const void* residual; int64_t ldr;
+  void* aux; int64_t ldaux;
+  int epilogue;
+  int force_simt; /* testing aid: run the SIMT kernel even for bf16 */
+} bp_gemm_args;
+BP_API int bp_gemm(const bp_gemm_args* args, void* stream);
+
+/* ----------------------------------------------------------- LayerNorm --
+ * y = (x - mean) * rstd * gamma + beta over `cols`; mean/rstd saved (fp32).
+ * bwd: dx = dres + dLN(dy)   (dres may be NULL); dgamma/dbeta += (fp32).
+ */
+BP_API int bp_layernorm_fwd(int dtype, int rows, int cols, const void* x, const void* gamma,
+                     const void* beta, float eps, void* y, float* mean, float* rstd,
+                     void* stream);
+BP_API int bp_layernorm_bwd(int dtype, int rows, int cols, const void* dy, const void* x,
+                     const void* gamma, const float* mean, const float* rstd,
+                     const void* dres, void* dx, float* dgamma, float* dbeta, void* stream);
+
+/* ------------------------------------------------------- elementwise --- */
+/* out[r, :] += sum over rows of x (fp32 accumulate into out[cols]). */
+BP_API int bp_colsum_acc(int dtype, int rows, int cols, const void* x, int64_t ldx, float* out,
+                  void* stream);
+/* out[b*S+s, :] = wte[tok[b*S+s], :] + wpe[s, :] */
+BP_API int bp_embed_fwd(int dtype, int B, int S, int H, const int32_t* tokens, const void* wte,
+                 const void* wpe, void* out, void* stream);
+/* dwte[tok] += dout ; dwpe[s] += sum_b dout  (fp32 grads) */
+BP_API int bp_embed_bwd(int dtype, int B, int S, int H, const int32_t* tokens, const void* dout,
+                 float* dwte, float* dwpe, void* stream);
+/* Fused softmax cross-entropy over V columns, in place:
+ * logits[r,:] <- (softmax(logits[r,:]) - onehot(target[r])) * grad_scale ;
+ * loss_out[0] += loss_scale * sum_r (logsumexp - logit[target]). */
+BP_API int bp_xent_fwd_bwd(int dtype, int rows, int V, void* logits, int64_t ld, const int32_t* targets,
+                    float grad_scale, float loss_scale, float* loss_out, void* stream);
+/* y = x (elementwise cast / copy), n elements */
+BP_API int bp_cast(int src_dtype, int dst_dtype, int64_t n, const void* src, void* dst, void* stream);
+
+/* ----------------------------------------------------------- attention --
+ * Multi-head attention over a packed QKV activation [B*S, 3*H*Dh]
+ * (columns: q heads | k heads | v heads, head-major within each).
+ * o: [B*S, H*Dh].  lse: [B*H*S] fp32 (saved for backward).
+ * bwd writes dqkv [B*S, 3*H*Dh]; workspace: bp_attn_workspace_bytes().
+ */
+BP_API int64_t bp_attn_workspace_bytes(int B, int S, int H, int Dh);
+BP_API int bp_attn_fwd(int dtype, int B, int S, int H, int Dh, int causal, float scale,
+                const void* qkv, void* o, float* lse, void* stream);
+BP_API int bp_attn_bwd(int dtype, int B, int S, int H, int Dh, int causal, float scale,
+                const void* qkv, const void* o, const void* dout, const float* lse,
+                void* dqkv, float* workspace, void* stream);
+
+/* -------------------------------------------------------------- Adam ----
+ * Fused replica-mean + AdamW on a flat parameter buffer of n elements.
+ *   g = (grad_a + grad_b) * 0.5   (grad_b may be NULL: g = grad_a)
+ *   g *= grad_scale
+ *   m = b1 m + (1-b1) g ; v = b2 v + (1-b2) g^2
+ *   master -= lr * ( mhat / (sqrt(vhat) + eps) + wd * master )
+ *   param_a, param_b (optional, param dtype) <- master
+ * The order of the replica sum is fixed (a then b) so every replica that
+ * performs the update computes bit-identical weights.
+ */
+BP_API int bp_adam(int64_t n, int param_dtype, float* master, const float* grad_a, const float* grad_b,
+            float* m, float* v, void* param_a, void* param_b, float lr, float beta1, float beta2,
+            float eps, float weight_decay, int step, float grad_scale, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BITPIPE_B200_H */

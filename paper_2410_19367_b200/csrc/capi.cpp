@@ -1,0 +1,79 @@
+// Library-wide state of libbitpipe_b200.so: thread-local error text, the
+// kernel launch counter, cached device properties and testing switches.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+
+#include "../../include/bitpipe.h"
+
+namespace bp {
+
+static thread_local char g_err[1024] = "";
+static std::atomic<unsigned long long> g_launches{0};
+static std::atomic<int> g_opt_attn_exact{0}, g_opt_gemm_simt{0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  set_error("CUDA error %d (%s) in %s", (int)e, cudaGetErrorString(e), what);
+  return BP_ERR_CUDA;
+}
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int num_sms() {
+  static thread_local int cached_dev = -1, cached = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cached;
+  if (dev != cached_dev) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0) cached = n;
+    cached_dev = dev;
+  }
+  return cached;
+}
+
+bool opt_attn_exact() { return g_opt_attn_exact.load() != 0; }
+bool opt_gemm_simt() { return g_opt_gemm_simt.load() != 0; }
+
+}  // namespace bp
+
+extern "C" {
+
+int bp_abi_version(void) { return BP_ABI_VERSION; }
+
+const char* bp_last_error(void) { return bp::g_err; }
+
+int bp_sm_count(int device) {
+  int n = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) return -bp::cuda_status(e, "cudaDeviceGetAttribute");
+  return n;
+}
+
+int bp_tc_available(void) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return (major == 10 && minor == 0) ? 1 : 0;
+}
+
+unsigned long long bp_launch_count(void) { return bp::g_launches.load(); }
+
+int bp_set_option(int option, int value) {
+  switch (option) {
+    case BP_OPT_ATTN_EXACT: bp::g_opt_attn_exact.store(value); return BP_OK;
+    case BP_OPT_GEMM_SIMT: bp::g_opt_gemm_simt.store(value); return BP_OK;
+    default: bp::set_error("bp_set_option: unknown option %d", option); return BP_ERR_INVALID;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,290 @@
+// Bandwidth kernels of the per-stage passes:
+// bias-gradient column sums, embedding fwd/bwd, fused softmax
+// cross-entropy fwd+bwd, dtype cast, fused replica-mean AdamW.
+#include "common.cuh"
+
+namespace bp {
+void count_launch();
+int num_sms();
+
+// ------------------------------------------------------------ colsum ----
+// out[c] += sum_r x[r, c]; thread per 2 columns, row chunks on grid.y.
+template <typename T>
+__global__ void colsum_kernel(int rows, int cols, const T* __restrict__ x, int64_t ld, int rows_per,
+                              float* __restrict__ out) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (c >= cols) return;
+  const int r0 = blockIdx.y * rows_per, r1 = min(rows, r0 + rows_per);
+  float a = 0.f, b = 0.f;
+  const bool two = c + 1 < cols;
+  for (int r = r0; r < r1; ++r) {
+    const T* p = x + (int64_t)r * ld + c;
+    a += to_f<T>(p[0]);
+    if (two) b += to_f<T>(p[1]);
+  }
+  atomicAdd(&out[c], a);
+  if (two) atomicAdd(&out[c + 1], b);
+}
+
+// ------------------------------------------------------------- embed ----
+template <typename T>
+__global__ void embed_fwd_kernel(int B, int S, int H, const int32_t* __restrict__ tok, const T* __restrict__ wte,
+                                 const T* __restrict__ wpe, T* __restrict__ out) {
+  const int r = blockIdx.x;  // token row b*S + s
+  const int s = r % S;
+  const int64_t t = tok[r];
+  for (int c = threadIdx.x; c < H; c += blockDim.x)
+    out[(int64_t)r * H + c] = from_f<T>(to_f<T>(wte[t * H + c]) + to_f<T>(wpe[(int64_t)s * H + c]));
+}
+
+template <typename T>
+__global__ void embed_bwd_tok_kernel(int H, const int32_t* __restrict__ tok, const T* __restrict__ dout,
+                                     float* __restrict__ dwte) {
+  const int r = blockIdx.x;
+  const int64_t t = tok[r];
+  for (int c = threadIdx.x; c < H; c += blockDim.x) atomicAdd(&dwte[t * H + c], to_f<T>(dout[(int64_t)r * H + c]));
+}
+
+template <typename T>
+__global__ void embed_bwd_pos_kernel(int B, int S, int H, const T* __restrict__ dout, float* __restrict__ dwpe) {
+  const int s = blockIdx.x;
+  for (int c = threadIdx.x; c < H; c += blockDim.x) {
+    float a = 0.f;
+    for (int b = 0; b < B; ++b) a += to_f<T>(dout[((int64_t)b * S + s) * H + c]);
+    dwpe[(int64_t)s * H + c] += a;
+  }
+}
+
+// --------------------------------------------------------------- xent ----
+// Block per row.  Pass 1: online max / sum-exp.  Pass 2: write the scaled
+// gradient in place.  Loss uses logsumexp - logit[target].
+template <typename T>
+__global__ void __launch_bounds__(512) xent_kernel(int V, T* __restrict__ logits, int64_t ld,
+                                                   const int32_t* __restrict__ tgt, float grad_scale,
+                                                   float loss_scale, float* __restrict__ loss) {
+  const int r = blockIdx.x;
+  T* row = logits + (int64_t)r * ld;
+  float m = -INFINITY, s = 0.f;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+    const float x = to_f<T>(row[c]);
+    if (x > m) {
+      s = s * __expf(m - x) + 1.f;
+      m = x;
+    } else {
+      s += __expf(x - m);
+    }
+  }
+  // combine (m, s) across the warp then the block
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const float mm = fmaxf(m, m2);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+    m = mm;
+  }
+  __shared__ float sm[32], ss[32];
+  __shared__ float g_m, g_lse;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sm[w] = m;
+    ss[w] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = -INFINITY;
+    const int nw = blockDim.x >> 5;
+    for (int i = 0; i < nw; ++i) M = fmaxf(M, sm[i]);
+    float S = 0.f;
+    for (int i = 0; i < nw; ++i) S += ss[i] == 0.f ? 0.f : ss[i] * __expf(sm[i] - M);
+    g_m = M;
+    g_lse = M + logf(S);
+    const int t = tgt[r];
+    atomicAdd(loss, loss_scale * (g_lse - to_f<T>(row[t])));
+  }
+  __syncthreads();
+  const float lse = g_lse;
+  const int t = tgt[r];
+  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+    const float p = __expf(to_f<T>(row[c]) - lse);
+    row[c] = from_f<T>((p - (c == t ? 1.f : 0.f)) * grad_scale);
+  }
+}
+
+// --------------------------------------------------------------- cast ----
+template <typename S, typename D>
+__global__ void cast_kernel(int64_t n, const S* __restrict__ src, D* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = from_f<D>(to_f<S>(src[i]));
+}
+
+// --------------------------------------------------------------- adam ----
+template <typename P>
+__global__ void adam_kernel(int64_t n, float* __restrict__ master, const float* __restrict__ ga,
+                            const float* __restrict__ gb, float* __restrict__ m, float* __restrict__ v,
+                            P* __restrict__ pa, P* __restrict__ pb, float lr, float b1, float b2, float eps, float wd,
+                            float bc1, float bc2, float gscale) {
+  const int64_t n4 = n / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 g = reinterpret_cast<const float4*>(ga)[i];
+    if (gb) {
+      const float4 h = reinterpret_cast<const float4*>(gb)[i];
+      g.x = (g.x + h.x) * 0.5f; g.y = (g.y + h.y) * 0.5f; g.z = (g.z + h.z) * 0.5f; g.w = (g.w + h.w) * 0.5f;
+    }
+    float4 w = reinterpret_cast<float4*>(master)[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    float gg[4] = {g.x, g.y, g.z, g.w}, ww[4] = {w.x, w.y, w.z, w.w};
+    float m4[4] = {mm.x, mm.y, mm.z, mm.w}, v4[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float gj = gg[j] * gscale;
+      m4[j] = b1 * m4[j] + (1.f - b1) * gj;
+      v4[j] = b2 * v4[j] + (1.f - b2) * gj * gj;
+      const float upd = (m4[j] / bc1) / (sqrtf(v4[j] / bc2) + eps) + wd * ww[j];
+      ww[j] -= lr * upd;
+    }
+    reinterpret_cast<float4*>(master)[i] = make_float4(ww[0], ww[1], ww[2], ww[3]);
+    reinterpret_cast<float4*>(m)[i] = make_float4(m4[0], m4[1], m4[2], m4[3]);
+    reinterpret_cast<float4*>(v)[i] = make_float4(v4[0], v4[1], v4[2], v4[3]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (pa) pa[4 * i + j] = from_f<P>(ww[j]);
+      if (pb) pb[4 * i + j] = from_f<P>(ww[j]);
+    }
+  }
+  // tail
+  for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    float g = ga[i];
+    if (gb) g = (g + gb[i]) * 0.5f;
+    g *= gscale;
+    m[i] = b1 * m[i] + (1.f - b1) * g;
+    v[i] = b2 * v[i] + (1.f - b2) * g * g;
+    const float w = master[i] - lr * ((m[i] / bc1) / (sqrtf(v[i] / bc2) + eps) + wd * master[i]);
+    master[i] = w;
+    if (pa) pa[i] = from_f<P>(w);
+    if (pb) pb[i] = from_f<P>(w);
+  }
+}
+
+static int grid_for(int64_t n, int per_block) {
+  int64_t g = (n + per_block - 1) / per_block;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace bp
+
+using namespace bp;
+
+extern "C" int bp_colsum_acc(int dtype, int rows, int cols, const void* x, int64_t ldx, float* out, void* stream) {
+  if (rows <= 0 || cols <= 0) {
+    set_error("colsum: bad shape");
+    return BP_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int cblocks = (cols + 511) / 512;
+  int chunks = (2 * num_sms() + cblocks - 1) / cblocks;
+  int rows_per = (rows + chunks - 1) / chunks;
+  if (rows_per < 8) rows_per = 8;
+  dim3 grid(cblocks, (rows + rows_per - 1) / rows_per);
+  if (dtype == BP_F32)
+    colsum_kernel<float><<<grid, 256, 0, st>>>(rows, cols, (const float*)x, ldx, rows_per, out);
+  else
+    colsum_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(rows, cols, (const __nv_bfloat16*)x, ldx, rows_per, out);
+  count_launch();
+  BP_CHECK_LAUNCH("colsum");
+  return BP_OK;
+}
+
+extern "C" int bp_embed_fwd(int dtype, int B, int S, int H, const int32_t* tokens, const void* wte, const void* wpe,
+                            void* out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int threads = H >= 256 ? 256 : 64;
+  if (dtype == BP_F32)
+    embed_fwd_kernel<float><<<B * S, threads, 0, st>>>(B, S, H, tokens, (const float*)wte, (const float*)wpe,
+                                                        (float*)out);
+  else
+    embed_fwd_kernel<__nv_bfloat16><<<B * S, threads, 0, st>>>(B, S, H, tokens, (const __nv_bfloat16*)wte,
+                                                                (const __nv_bfloat16*)wpe, (__nv_bfloat16*)out);
+  count_launch();
+  BP_CHECK_LAUNCH("embed_fwd");
+  return BP_OK;
+}
+
+extern "C" int bp_embed_bwd(int dtype, int B, int S, int H, const int32_t* tokens, const void* dout, float* dwte,
+                            float* dwpe, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int threads = H >= 256 ? 256 : 64;
+  if (dtype == BP_F32) {
+    embed_bwd_tok_kernel<float><<<B * S, threads, 0, st>>>(H, tokens, (const float*)dout, dwte);
+    embed_bwd_pos_kernel<float><<<S, threads, 0, st>>>(B, S, H, (const float*)dout, dwpe);
+  } else {
+    embed_bwd_tok_kernel<__nv_bfloat16><<<B * S, threads, 0, st>>>(H, tokens, (const __nv_bfloat16*)dout, dwte);
+    embed_bwd_pos_kernel<__nv_bfloat16><<<S, threads, 0, st>>>(B, S, H, (const __nv_bfloat16*)dout, dwpe);
+  }
+  count_launch();
+  count_launch();
+  BP_CHECK_LAUNCH("embed_bwd");
+  return BP_OK;
+}
+
+extern "C" int bp_xent_fwd_bwd(int dtype, int rows, int V, void* logits, int64_t ld, const int32_t* targets,
+                               float grad_scale, float loss_scale, float* loss_out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int threads = V >= 4096 ? 512 : 128;
+  if (dtype == BP_F32)
+    xent_kernel<float><<<rows, threads, 0, st>>>(V, (float*)logits, ld, targets, grad_scale, loss_scale, loss_out);
+  else
+    xent_kernel<__nv_bfloat16><<<rows, threads, 0, st>>>(V, (__nv_bfloat16*)logits, ld, targets, grad_scale,
+                                                          loss_scale, loss_out);
+  count_launch();
+  BP_CHECK_LAUNCH("xent");
+  return BP_OK;
+}
+
+extern "C" int bp_cast(int sd, int dd, int64_t n, const void* src, void* dst, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int g = grid_for(n, 256 * 4);
+  if (sd == BP_F32 && dd == BP_BF16)
+    cast_kernel<float, __nv_bfloat16><<<g, 256, 0, st>>>(n, (const float*)src, (__nv_bfloat16*)dst);
+  else if (sd == BP_BF16 && dd == BP_F32)
+    cast_kernel<__nv_bfloat16, float><<<g, 256, 0, st>>>(n, (const __nv_bfloat16*)src, (float*)dst);
+  else if (sd == BP_F32 && dd == BP_F32)
+    cast_kernel<float, float><<<g, 256, 0, st>>>(n, (const float*)src, (float*)dst);
+  else
+    cast_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, st>>>(n, (const __nv_bfloat16*)src, (__nv_bfloat16*)dst);
+  count_launch();
+  BP_CHECK_LAUNCH("cast");
+  return BP_OK;
+}
+
+extern "C" int bp_adam(int64_t n, int param_dtype, float* master, const float* grad_a, const float* grad_b, float* m,
+                       float* v, void* param_a, void* param_b, float lr, float beta1, float beta2, float eps,
+                       float weight_decay, int step, float grad_scale, void* stream) {
+  if (n <= 0 || step < 1) {
+    set_error("adam: bad n/step");
+    return BP_ERR_INVALID;
+  }
+  if ((reinterpret_cast<uintptr_t>(master) | reinterpret_cast<uintptr_t>(grad_a) |
+       reinterpret_cast<uintptr_t>(grad_b) | reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 15) {
+    set_error("adam: fp32 buffers must be 16-byte aligned");
+    return BP_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
+  const int g = grid_for(n / 4 + 1, 256);
+  if (param_dtype == BP_F32)
+    adam_kernel<float><<<g, 256, 0, st>>>(n, master, grad_a, grad_b, m, v, (float*)param_a, (float*)param_b, lr, beta1,
+                                          beta2, eps, weight_decay, bc1, bc2, grad_scale);
+  else
+    adam_kernel<__nv_bfloat16><<<g, 256, 0, st>>>(n, master, grad_a, grad_b, m, v, (__nv_bfloat16*)param_a,
+                                                  (__nv_bfloat16*)param_b, lr, beta1, beta2, eps, weight_decay, bc1,
+                                                  bc2, grad_scale);
+  count_launch();
+  BP_CHECK_LAUNCH("adam");
+  return BP_OK;
+}

@@ -1,0 +1,479 @@
+// GEMM for the per-virtual-stage transformer passes.
+//
+// bf16: persistent warp-specialised tcgen05 kernel.
+//   * 128 x BN x 64 tiles (BN = 256 or 128), 4-6 stage TMA -> smem ring
+//     (SWIZZLE_128B), fp32 accumulators in TMEM, double-buffered so the
+//     epilogue of tile i overlaps the MMAs of tile i+1.
+//   * warp 0: TMA producer (one elected lane), warp 1: MMA issuer (one
+//     lane issues tcgen05.mma, tcgen05.commit frees smem slots / signals
+//     the epilogue), warp 2: TMEM allocator, warps 4-7: epilogue
+//     (tcgen05.ld 32x32b -> registers -> fused bias / GELU / dGELU /
+//     residual / fp32-accumulate -> global).
+//   * A and B may each be K-major or MN-major; the smem descriptors and
+//     the instruction descriptor's transpose bits absorb the layout, so
+//     fprop (X W^T), dgrad (dY W) and wgrad (dY^T X) run without any
+//     explicit transpose.
+// fp32: exact-fp32 SIMT kernel (check mode; no TF32) with the same epilogue.
+#include "common.cuh"
+
+#include <mutex>
+
+namespace bp {
+
+struct Epi {
+  int M, N;
+  void* C;
+  int64_t ldc;
+  int c_dtype;
+  float alpha;
+  int accumulate;
+  const void* bias;
+  int bias_dtype;
+  const void* residual;
+  int64_t ldr;
+  void* aux;
+  int64_t ldaux;
+  int epilogue;
+  int vec_ok;
+};
+
+BP_DEV float ld_any(const void* p, int dtype, int64_t i) {
+  return dtype == BP_F32 ? static_cast<const float*>(p)[i]
+                         : __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
+}
+BP_DEV void st_any(void* p, int dtype, int64_t i, float v) {
+  if (dtype == BP_F32)
+    static_cast<float*>(p)[i] = v;
+  else
+    static_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(v);
+}
+
+// Scalar epilogue for one element (used by the SIMT kernel and ragged tiles).
+BP_DEV void epi_one(const Epi& ep, int r, int c, float acc) {
+  float v = acc * ep.alpha;
+  if (ep.bias) v += ld_any(ep.bias, ep.bias_dtype, c);
+  if (ep.epilogue == BP_EPI_GELU) {
+    st_any(ep.aux, ep.c_dtype, (int64_t)r * ep.ldaux + c, v);
+    // GELU is applied to the value as stored (rounded) so fwd/bwd agree.
+    v = gelu_f(ld_any(ep.aux, ep.c_dtype, (int64_t)r * ep.ldaux + c));
+  } else if (ep.epilogue == BP_EPI_DGELU) {
+    v *= gelu_grad_f(ld_any(ep.aux, ep.c_dtype, (int64_t)r * ep.ldaux + c));
+  }
+  if (ep.residual) v += ld_any(ep.residual, ep.c_dtype, (int64_t)r * ep.ldr + c);
+  int64_t o = (int64_t)r * ep.ldc + c;
+  if (ep.accumulate) v += static_cast<const float*>(ep.C)[o];
+  st_any(ep.C, ep.c_dtype, o, v);
+}
+
+// 32 consecutive columns of one row, vectorised (16-byte accesses).
+BP_DEV void load32(const void* p, int dtype, int64_t off, float (&x)[32]) {
+  if (dtype == BP_F32) {
+    const float4* q = reinterpret_cast<const float4*>(static_cast<const float*>(p) + off);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float4 t = q[i];
+      x[4 * i] = t.x; x[4 * i + 1] = t.y; x[4 * i + 2] = t.z; x[4 * i + 3] = t.w;
+    }
+  } else {
+    const uint4* q = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p) + off);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint4 t = q[i];
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&t);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 f = __bfloat1622float2(h[j]);
+        x[8 * i + 2 * j] = f.x;
+        x[8 * i + 2 * j + 1] = f.y;
+      }
+    }
+  }
+}
+BP_DEV void store32(void* p, int dtype, int64_t off, const float (&x)[32]) {
+  if (dtype == BP_F32) {
+    float4* q = reinterpret_cast<float4*>(static_cast<float*>(p) + off);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] = make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]);
+  } else {
+    uint4* q = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p) + off);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint4 t;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&t);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(x[8 * i + 2 * j], x[8 * i + 2 * j + 1]);
+      q[i] = t;
+    }
+  }
+}
+
+BP_DEV void epi_row32(const Epi& ep, int r, int c0, float (&v)[32]) {
+  if (r >= ep.M) return;
+  if (!ep.vec_ok || c0 + 32 > ep.N) {
+    for (int i = 0; i < 32 && c0 + i < ep.N; ++i) epi_one(ep, r, c0 + i, v[i]);
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] *= ep.alpha;
+  float t[32];
+  if (ep.bias) {
+    load32(ep.bias, ep.bias_dtype, c0, t);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] += t[i];
+  }
+  if (ep.epilogue == BP_EPI_GELU) {
+    const int64_t ao = (int64_t)r * ep.ldaux + c0;
+    store32(ep.aux, ep.c_dtype, ao, v);
+    if (ep.c_dtype == BP_BF16) {  // gelu of the rounded pre-activation
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i]);
+  } else if (ep.epilogue == BP_EPI_DGELU) {
+    load32(ep.aux, ep.c_dtype, (int64_t)r * ep.ldaux + c0, t);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(t[i]);
+  }
+  if (ep.residual) {
+    load32(ep.residual, ep.c_dtype, (int64_t)r * ep.ldr + c0, t);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] += t[i];
+  }
+  const int64_t o = (int64_t)r * ep.ldc + c0;
+  if (ep.accumulate) {
+    load32(ep.C, BP_F32, o, t);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] += t[i];
+  }
+  store32(ep.C, ep.c_dtype, o, v);
+}
+
+// ===================================================== tcgen05 kernel ====
+template <int BN>
+struct TcCfg {
+  static constexpr int BM = 128, BK = 64;
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr uint32_t A_BYTES = BM * BK * 2;
+  static constexpr uint32_t B_BYTES = BN * BK * 2;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;  // two fp32 accumulators
+  static constexpr size_t SMEM = 1024 + STAGES * (size_t)STAGE_BYTES + 256;
+};
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(256, 1)
+gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+               int M, int N, int K, Epi ep) {
+  using C = TcCfg<BN>;
+  constexpr int BM = C::BM, BK = C::BK, STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int kblocks = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------------------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (tile % tiles_m) * BM, n0 = (tile / tiles_m) * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* a = sA + stage * C::A_BYTES;
+          uint8_t* b = sB + stage * C::B_BYTES;
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_2d(a, &map_a, k0, m0, &full[stage]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c) tma_load_2d(a + c * (BK * 128), &map_a, m0 + 64 * c, k0, &full[stage]);
+          }
+          if (!B_MN) {
+            tma_load_2d(b, &map_b, k0, n0, &full[stage]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c) tma_load_2d(b + c * (BK * 128), &map_b, n0 + 64 * c, k0, &full[stage]);
+          }
+          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------------------------- MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(128, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? umma_desc_sw128(a_addr + k * 2048, BK * 128, 1024)
+                                     : umma_desc_sw128(a_addr + k * 32, 0, 1024);
+            const uint64_t bd = B_MN ? umma_desc_sw128(b_addr + k * 2048, BK * 128, 1024)
+                                     : umma_desc_sw128(b_addr + k * 32, 0, 1024);
+            tc_mma_f16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {  // ------------------------------ epilogue
+    const int ew = warp - 4;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      const int m0 = (tile % tiles_m) * BM, n0 = (tile / tiles_m) * BN;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m0 + ew * 32 + lane;
+      const uint32_t t0 = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        tmem_ld_32x32b_x32(t0 + c * 32, v);
+        if (n0 + c * 32 < N) epi_row32(ep, row, n0 + c * 32, v);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
+}
+
+// ======================================================== SIMT kernel ====
+// 64x64 tile, 256 threads x (4x4) outputs, fp32 FFMA accumulate.
+template <typename T>
+__global__ void __launch_bounds__(256)
+gemm_simt_kernel(int M, int N, int K, const T* __restrict__ A, int64_t lda, int a_kmajor,
+                 const T* __restrict__ B, int64_t ldb, int b_kmajor, Epi ep) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = threadIdx.x; i < 16 * 64; i += 256) {
+      int kk, mm;
+      if (a_kmajor) { kk = i % 16; mm = i / 16; } else { mm = i % 64; kk = i / 64; }
+      const int gm = m0 + mm, gk = k0 + kk;
+      float va = 0.f;
+      if (gm < M && gk < K) va = to_f<T>(a_kmajor ? A[(int64_t)gm * lda + gk] : A[(int64_t)gk * lda + gm]);
+      As[kk][mm] = va;
+      int nn;
+      if (b_kmajor) { kk = i % 16; nn = i / 16; } else { nn = i % 64; kk = i / 64; }
+      const int gn = n0 + nn;
+      const int gk2 = k0 + kk;
+      float vb = 0.f;
+      if (gn < N && gk2 < K) vb = to_f<T>(b_kmajor ? B[(int64_t)gn * ldb + gk2] : B[(int64_t)gk2 * ldb + gn]);
+      Bs[kk][nn] = vb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = m0 + ty * 4 + i, c = n0 + tx * 4 + j;
+      if (r < M && c < N) epi_one(ep, r, c, acc[i][j]);
+    }
+}
+
+// ============================================================== host ======
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// bf16 2-D map over a row-major matrix with `inner` contiguous elements per
+// row (row pitch `ld` elements) and `outer` rows; box = box_inner x box_outer.
+static int make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, int64_t ld,
+                    uint32_t box_inner, uint32_t box_outer) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return BP_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu ld=%lld box=%ux%u", (int)r,
+              (unsigned long long)inner, (unsigned long long)outer, (long long)ld, box_inner, box_outer);
+    return BP_ERR_INVALID;
+  }
+  return BP_OK;
+}
+
+void count_launch();
+int num_sms();
+bool opt_gemm_simt();
+
+template <int BN, bool A_MN, bool B_MN>
+static int launch_tc(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
+  using C = TcCfg<BN>;
+  CUtensorMap ma, mb;
+  int rc;
+  if (!A_MN)
+    rc = make_map(&ma, g.A, g.K, g.M, g.lda, 64, 128);
+  else
+    rc = make_map(&ma, g.A, g.M, g.K, g.lda, 64, 64);
+  if (rc) return rc;
+  if (!B_MN)
+    rc = make_map(&mb, g.B, g.K, g.N, g.ldb, 64, BN);
+  else
+    rc = make_map(&mb, g.B, g.N, g.K, g.ldb, 64, 64);
+  if (rc) return rc;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    BP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr_set = true;
+  }
+  const int tiles = ((g.M + 127) / 128) * ((g.N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, 256, C::SMEM, st>>>(ma, mb, g.M, g.N, g.K, ep);
+  count_launch();
+  BP_CHECK_LAUNCH("gemm_tc");
+  return BP_OK;
+}
+
+template <int BN>
+static int dispatch_tc(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
+  const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
+  if (!amn && !bmn) return launch_tc<BN, false, false>(g, ep, st);
+  if (!amn && bmn) return launch_tc<BN, false, true>(g, ep, st);
+  if (amn && !bmn) return launch_tc<BN, true, false>(g, ep, st);
+  return launch_tc<BN, true, true>(g, ep, st);
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace bp
+
+using namespace bp;
+
+extern "C" int bp_gemm(const bp_gemm_args* gp, void* stream) {
+  if (!gp) {
+    set_error("bp_gemm: null args");
+    return BP_ERR_INVALID;
+  }
+  const bp_gemm_args& g = *gp;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0) {
+    set_error("bp_gemm: bad shape M=%d N=%d K=%d", g.M, g.N, g.K);
+    return BP_ERR_INVALID;
+  }
+  if (g.beta != 0.f && (g.beta != 1.f || g.c_dtype != BP_F32)) {
+    set_error("bp_gemm: beta must be 0, or 1 with an fp32 C");
+    return BP_ERR_INVALID;
+  }
+  if ((g.epilogue == BP_EPI_GELU || g.epilogue == BP_EPI_DGELU) && !g.aux) {
+    set_error("bp_gemm: GELU epilogues need aux");
+    return BP_ERR_INVALID;
+  }
+  Epi ep;
+  ep.M = g.M; ep.N = g.N; ep.C = g.C; ep.ldc = g.ldc; ep.c_dtype = g.c_dtype; ep.alpha = g.alpha;
+  ep.accumulate = g.beta != 0.f; ep.bias = g.bias; ep.bias_dtype = g.in_dtype;
+  ep.residual = g.residual; ep.ldr = g.ldr; ep.aux = g.aux; ep.ldaux = g.ldaux; ep.epilogue = g.epilogue;
+  const int esz = g.c_dtype == BP_F32 ? 4 : 2;
+  ep.vec_ok = aligned16(g.C) && (g.ldc * esz) % 16 == 0 && (!g.bias || aligned16(g.bias)) &&
+              (!g.residual || (aligned16(g.residual) && (g.ldr * esz) % 16 == 0)) &&
+              (!g.aux || (aligned16(g.aux) && (g.ldaux * esz) % 16 == 0));
+  if (g.in_dtype == BP_BF16 && !g.force_simt && !opt_gemm_simt()) {
+    const bool ok = aligned16(g.A) && aligned16(g.B) && (g.lda % 8) == 0 && (g.ldb % 8) == 0;
+    if (!ok) {
+      set_error("bp_gemm: bf16 operands need 16-byte aligned bases and ld %% 8 == 0");
+      return BP_ERR_INVALID;
+    }
+    const int tiles256 = ((g.M + 127) / 128) * ((g.N + 255) / 256);
+    if (g.N > 128 && tiles256 >= num_sms()) return dispatch_tc<256>(g, ep, st);
+    return dispatch_tc<128>(g, ep, st);
+  }
+  dim3 grid((g.N + 63) / 64, (g.M + 63) / 64);
+  if (g.in_dtype == BP_F32)
+    gemm_simt_kernel<float><<<grid, 256, 0, st>>>(g.M, g.N, g.K, static_cast<const float*>(g.A), g.lda, g.a_kmajor,
+                                                   static_cast<const float*>(g.B), g.ldb, g.b_kmajor, ep);
+  else
+    gemm_simt_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+        g.M, g.N, g.K, static_cast<const __nv_bfloat16*>(g.A), g.lda, g.a_kmajor,
+        static_cast<const __nv_bfloat16*>(g.B), g.ldb, g.b_kmajor, ep);
+  count_launch();
+  BP_CHECK_LAUNCH("gemm_simt");
+  return BP_OK;
+}

@@ -1,0 +1,341 @@
+// LayerNorm forward/backward -- HBM-bound.
+//
+// Fast path (bf16 or fp32, cols % (32*VEC) == 0, cols <= 4096): one warp per
+// row, the row held in registers as packed 16-byte vectors, two-pass mean /
+// variance from registers, warp-shuffle reductions.  dgamma/dbeta are
+// column sums over rows: a coalesced column kernel (thread per column,
+// row chunks spread over the GPU, one fp32 atomicAdd per chunk).
+// Generic path (any shape): block per row.
+#include "common.cuh"
+
+namespace bp {
+void count_launch();
+int num_sms();
+
+template <typename T>
+struct Vec;  // 16-byte vector of T
+template <>
+struct Vec<float> {
+  static constexpr int N = 4;
+  using U = float4;
+  BP_DEV static void unpack(const U& u, float* f) { f[0] = u.x; f[1] = u.y; f[2] = u.z; f[3] = u.w; }
+  BP_DEV static U pack(const float* f) { return make_float4(f[0], f[1], f[2], f[3]); }
+};
+template <>
+struct Vec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  using U = uint4;
+  BP_DEV static void unpack(const U& u, float* f) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 t = __bfloat1622float2(h[j]);
+      f[2 * j] = t.x;
+      f[2 * j + 1] = t.y;
+    }
+  }
+  BP_DEV static U pack(const float* f) {
+    U u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+    return u;
+  }
+};
+
+// ------------------------------------------------------------ fast path --
+template <typename T, int NV>  // NV vectors per lane; cols = 32 * NV * Vec::N
+__global__ void __launch_bounds__(256) ln_fwd_warp(int rows, const T* __restrict__ x, const T* __restrict__ g,
+                                                   const T* __restrict__ b, float eps, T* __restrict__ y,
+                                                   float* __restrict__ mean, float* __restrict__ rstd) {
+  using V = Vec<T>;
+  constexpr int E = V::N;
+  constexpr int cols = 32 * NV * E;
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const typename V::U* xr = reinterpret_cast<const typename V::U*>(x + (int64_t)row * cols);
+  typename V::U pv[NV];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    pv[i] = xr[i * 32 + lane];
+    float t[E];
+    V::unpack(pv[i], t);
+#pragma unroll
+    for (int j = 0; j < E; ++j) s += t[j];
+  }
+  const float mu = warp_sum(s) * (1.f / cols);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float t[E];
+    V::unpack(pv[i], t);
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      float d = t[j] - mu;
+      q += d * d;
+    }
+  }
+  const float rs = rsqrtf(warp_sum(q) * (1.f / cols) + eps);
+  const typename V::U* gr = reinterpret_cast<const typename V::U*>(g);
+  const typename V::U* br = reinterpret_cast<const typename V::U*>(b);
+  typename V::U* yr = reinterpret_cast<typename V::U*>(y + (int64_t)row * cols);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float gg[E], bb[E], o[E], t[E];
+    V::unpack(pv[i], t);
+    V::unpack(gr[i * 32 + lane], gg);
+    V::unpack(br[i * 32 + lane], bb);
+#pragma unroll
+    for (int j = 0; j < E; ++j) o[j] = (t[j] - mu) * rs * gg[j] + bb[j];
+    yr[i * 32 + lane] = V::pack(o);
+  }
+  if (lane == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+}
+
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) ln_bwd_warp(int rows, const T* __restrict__ dy, const T* __restrict__ x,
+                                                   const T* __restrict__ g, const float* __restrict__ mean,
+                                                   const float* __restrict__ rstd, const T* __restrict__ dres,
+                                                   T* __restrict__ dx) {
+  // dx only; dgamma/dbeta come from the coalesced column kernel below.
+  using V = Vec<T>;
+  using U = typename V::U;
+  constexpr int E = V::N;
+  constexpr int cols = 32 * NV * E;
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const U* dyr = reinterpret_cast<const U*>(dy + (int64_t)row * cols);
+  const U* xr = reinterpret_cast<const U*>(x + (int64_t)row * cols);
+  const U* gr = reinterpret_cast<const U*>(g);
+  const float mu = mean[row], rs = rstd[row];
+  U pa[NV], pd[NV], pg[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    pa[i] = xr[i * 32 + lane];
+    pd[i] = dyr[i * 32 + lane];
+    pg[i] = gr[i * 32 + lane];
+  }
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float a[E], d[E], gg[E];
+    V::unpack(pa[i], a);
+    V::unpack(pd[i], d);
+    V::unpack(pg[i], gg);
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const float dh = d[j] * gg[j];
+      s1 += dh;
+      s2 += dh * (a[j] - mu) * rs;
+    }
+  }
+  s1 = warp_sum(s1) * (1.f / cols);
+  s2 = warp_sum(s2) * (1.f / cols);
+  U* dxr = reinterpret_cast<U*>(dx + (int64_t)row * cols);
+  const U* rr = dres ? reinterpret_cast<const U*>(dres + (int64_t)row * cols) : nullptr;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float a[E], d[E], gg[E], r[E], o[E];
+    V::unpack(pa[i], a);
+    V::unpack(pd[i], d);
+    V::unpack(pg[i], gg);
+    if (rr) V::unpack(rr[i * 32 + lane], r);
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const float xh = (a[j] - mu) * rs;
+      o[j] = rs * (d[j] * gg[j] - s1 - xh * s2) + (rr ? r[j] : 0.f);
+    }
+    dxr[i * 32 + lane] = V::pack(o);
+  }
+}
+
+// ---------------------------------------------------------- generic path --
+template <typename T>
+__global__ void ln_fwd_generic(int cols, const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b,
+                               float eps, T* __restrict__ y, float* __restrict__ mean, float* __restrict__ rstd) {
+  const int row = blockIdx.x;
+  const T* xr = x + (int64_t)row * cols;
+  __shared__ float sh[32];
+  __shared__ float stat;
+  float s = 0.f;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) s += to_f<T>(xr[c]);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    stat = t / cols;
+  }
+  __syncthreads();
+  const float mu = stat;
+  float q = 0.f;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    float d = to_f<T>(xr[c]) - mu;
+    q += d * d;
+  }
+  q = warp_sum(q);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = q;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    stat = rsqrtf(t / cols + eps);
+    mean[row] = mu;
+    rstd[row] = stat;
+  }
+  __syncthreads();
+  const float rs = stat;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x)
+    y[(int64_t)row * cols + c] = from_f<T>((to_f<T>(xr[c]) - mu) * rs * to_f<T>(g[c]) + to_f<T>(b[c]));
+}
+
+template <typename T>
+__global__ void ln_bwd_generic_dx(int cols, const T* __restrict__ dy, const T* __restrict__ x,
+                                  const T* __restrict__ g, const float* __restrict__ mean,
+                                  const float* __restrict__ rstd, const T* __restrict__ dres, T* __restrict__ dx) {
+  const int row = blockIdx.x;
+  const float mu = mean[row], rs = rstd[row];
+  const T* xr = x + (int64_t)row * cols;
+  const T* dr = dy + (int64_t)row * cols;
+  __shared__ float sh1[32], sh2[32];
+  __shared__ float m1, m2;
+  float s1 = 0.f, s2 = 0.f;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    float xh = (to_f<T>(xr[c]) - mu) * rs;
+    float dh = to_f<T>(dr[c]) * to_f<T>(g[c]);
+    s1 += dh;
+    s2 += dh * xh;
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if ((threadIdx.x & 31) == 0) {
+    sh1[threadIdx.x >> 5] = s1;
+    sh2[threadIdx.x >> 5] = s2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float a = 0.f, b = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += sh1[w];
+      b += sh2[w];
+    }
+    m1 = a / cols;
+    m2 = b / cols;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    float xh = (to_f<T>(xr[c]) - mu) * rs;
+    float dh = to_f<T>(dr[c]) * to_f<T>(g[c]);
+    float o = rs * (dh - m1 - xh * m2);
+    if (dres) o += to_f<T>(dres[(int64_t)row * cols + c]);
+    dx[(int64_t)row * cols + c] = from_f<T>(o);
+  }
+}
+
+// dgamma[c] += sum_r dy*xhat ; dbeta[c] += sum_r dy.  grid.x over columns,
+// grid.y over row chunks.
+template <typename T>
+__global__ void ln_bwd_generic_params(int rows, int cols, int rows_per, const T* __restrict__ dy,
+                                      const T* __restrict__ x, const float* __restrict__ mean,
+                                      const float* __restrict__ rstd, float* __restrict__ dgamma,
+                                      float* __restrict__ dbeta) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  const int r0 = blockIdx.y * rows_per, r1 = min(rows, r0 + rows_per);
+  float a = 0.f, b = 0.f;
+  for (int r = r0; r < r1; ++r) {
+    float d = to_f<T>(dy[(int64_t)r * cols + c]);
+    a += d * (to_f<T>(x[(int64_t)r * cols + c]) - mean[r]) * rstd[r];
+    b += d;
+  }
+  atomicAdd(&dgamma[c], a);
+  atomicAdd(&dbeta[c], b);
+}
+
+template <typename T>
+static int ln_fwd_t(int rows, int cols, const void* x, const void* g, const void* b, float eps, void* y, float* mean,
+                    float* rstd, cudaStream_t st) {
+  constexpr int E = Vec<T>::N;
+  const int nv = cols % (32 * E) == 0 ? cols / (32 * E) : 0;
+  const dim3 grid((rows + 7) / 8);
+  const T *X = (const T*)x, *G = (const T*)g, *Bb = (const T*)b;
+  T* Y = (T*)y;
+  switch (nv) {
+#define BP_LNF(n) \
+  case n: ln_fwd_warp<T, n><<<grid, 256, 0, st>>>(rows, X, G, Bb, eps, Y, mean, rstd); break;
+    BP_LNF(1) BP_LNF(2) BP_LNF(3) BP_LNF(4) BP_LNF(5) BP_LNF(6) BP_LNF(8) BP_LNF(12) BP_LNF(16)
+#undef BP_LNF
+    default: ln_fwd_generic<T><<<rows, 256, 0, st>>>(cols, X, G, Bb, eps, Y, mean, rstd);
+  }
+  count_launch();
+  BP_CHECK_LAUNCH("ln_fwd");
+  return BP_OK;
+}
+
+template <typename T>
+static int ln_bwd_t(int rows, int cols, const void* dy, const void* x, const void* g, const float* mean,
+                    const float* rstd, const void* dres, void* dx, float* dgamma, float* dbeta, cudaStream_t st) {
+  constexpr int E = Vec<T>::N;
+  const int nv = cols % (32 * E) == 0 ? cols / (32 * E) : 0;
+  const T *DY = (const T*)dy, *X = (const T*)x, *G = (const T*)g, *R = (const T*)dres;
+  T* DX = (T*)dx;
+  switch (nv) {
+#define BP_LNB(n)                                                                                       \
+  case n:                                                                                               \
+    ln_bwd_warp<T, n><<<(rows + 7) / 8, 256, 0, st>>>(rows, DY, X, G, mean, rstd, R, DX);             \
+    break;
+    BP_LNB(1) BP_LNB(2) BP_LNB(3) BP_LNB(4) BP_LNB(5) BP_LNB(6) BP_LNB(8) BP_LNB(12) BP_LNB(16)
+#undef BP_LNB
+    default:
+      ln_bwd_generic_dx<T><<<rows, 256, 0, st>>>(cols, DY, X, G, mean, rstd, R, DX);
+  }
+  count_launch();
+  {
+    // column sums for dgamma / dbeta: enough row chunks to fill the GPU
+    int chunks = (2 * num_sms() * 256 + cols - 1) / cols;
+    if (chunks < 1) chunks = 1;
+    int rows_per = (rows + chunks - 1) / chunks;
+    if (rows_per < 16) rows_per = 16;
+    dim3 grid((cols + 255) / 256, (rows + rows_per - 1) / rows_per);
+    ln_bwd_generic_params<T><<<grid, 256, 0, st>>>(rows, cols, rows_per, DY, X, mean, rstd, dgamma, dbeta);
+    count_launch();
+  }
+  BP_CHECK_LAUNCH("ln_bwd");
+  return BP_OK;
+}
+
+}  // namespace bp
+
+using namespace bp;
+
+extern "C" int bp_layernorm_fwd(int dtype, int rows, int cols, const void* x, const void* gamma, const void* beta,
+                                float eps, void* y, float* mean, float* rstd, void* stream) {
+  if (rows <= 0 || cols <= 0) {
+    set_error("layernorm_fwd: bad shape");
+    return BP_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  return dtype == BP_F32 ? ln_fwd_t<float>(rows, cols, x, gamma, beta, eps, y, mean, rstd, st)
+                         : ln_fwd_t<__nv_bfloat16>(rows, cols, x, gamma, beta, eps, y, mean, rstd, st);
+}
+
+extern "C" int bp_layernorm_bwd(int dtype, int rows, int cols, const void* dy, const void* x, const void* gamma,
+                                const float* mean, const float* rstd, const void* dres, void* dx, float* dgamma,
+                                float* dbeta, void* stream) {
+  if (rows <= 0 || cols <= 0) {
+    set_error("layernorm_bwd: bad shape");
+    return BP_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  return dtype == BP_F32
+             ? ln_bwd_t<float>(rows, cols, dy, x, gamma, mean, rstd, dres, dx, dgamma, dbeta, st)
+             : ln_bwd_t<__nv_bfloat16>(rows, cols, dy, x, gamma, mean, rstd, dres, dx, dgamma, dbeta, st);
+}

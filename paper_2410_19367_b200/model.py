@@ -1,0 +1,190 @@
+"""Model family, parameter layout and the layer -> virtual-stage partitioner.
+
+The reference has no layer partitioner (SPEC.md:219 lists it as a non-goal)
+and no model: its train step is specified on a toy MLP.
+The north star fixes the model family instead: a GPT-style (causal) or
+BERT-style (bidirectional attention) pre-LN transformer.  Choices, stated
+once here and restated in ``oracle/gpt_oracle.py``:
+
+  * learned token + position embeddings; untied LM head (no bias);
+  * pre-LN blocks: x += proj(attn(LN1 x)); x += fc2(gelu_tanh(fc1(LN2 x)));
+    FFN = 4h; final LN before the head;
+  * loss = mean token cross-entropy per micro-batch; the step objective is
+    the mean over the N micro-batches (each replica averages its own N/2,
+    the replica pair averages);
+  * init: N(0, 0.02) weights, output projections N(0, 0.02/sqrt(2L)),
+    zero biases, unit LN gains (``perturb=True`` adds small noise to biases
+    and LN params so parity tests exercise every gradient).
+
+Partition: the 2L half-blocks (attention half, MLP half)
+are split over the v*D virtual stages of one direction in contiguous runs;
+stage 0 additionally owns the embedding and stage v*D-1 the final LN, LM
+head and loss.  In the V map both sit on device 0 (down) / D-1 (up).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+__all__ = ["ModelConfig", "CONFIGS", "StagePlan", "stage_partition", "param_specs", "stage_param_names",
+           "init_params", "flops_per_token"]
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    name: str
+    layers: int
+    hidden: int
+    heads: int
+    seq: int
+    vocab: int
+    micro_batch: int = 1
+    causal: bool = True
+    ffn_mult: int = 4
+    ln_eps: float = 1e-5
+
+    @property
+    def head_dim(self) -> int:
+        return self.hidden // self.heads
+
+    @property
+    def ffn(self) -> int:
+        return self.ffn_mult * self.hidden
+
+    @property
+    def tokens_per_microbatch(self) -> int:
+        return self.micro_batch * self.seq
+
+    def n_params(self) -> int:
+        return sum(math.prod(s) for _, s, _ in param_specs(self))
+
+
+CONFIGS = {
+    # BASELINE.json configs (SURVEY §8(d) hyper-parameters)
+    "tiny": ModelConfig("tiny-gpt", layers=4, hidden=64, heads=4, seq=32, vocab=256, micro_batch=2),
+    "bert-large": ModelConfig("bert-large", layers=24, hidden=1024, heads=16, seq=512, vocab=30528,
+                              micro_batch=4, causal=False),
+    "gpt-1.3b": ModelConfig("gpt-1.3b", layers=24, hidden=2048, heads=16, seq=2048, vocab=50304, micro_batch=1),
+    "gpt-10b": ModelConfig("gpt-10b", layers=48, hidden=4096, heads=32, seq=2048, vocab=50304, micro_batch=1),
+    # small configs used by tests
+    "small": ModelConfig("small-gpt", layers=4, hidden=256, heads=4, seq=128, vocab=512, micro_batch=2),
+    "small-bert": ModelConfig("small-bert", layers=2, hidden=128, heads=2, seq=64, vocab=300, micro_batch=2,
+                              causal=False),
+}
+
+
+def flops_per_token(cfg: ModelConfig) -> float:
+    """Megatron convention, no recompute, full (non-causal-discounted)
+    attention: 3 * (24 L h^2 + 4 s L h + 2 V h)."""
+    L, h, s, V = cfg.layers, cfg.hidden, cfg.seq, cfg.vocab
+    return 3.0 * (24 * L * h * h + 4 * s * L * h + 2 * V * h)
+
+
+@dataclass(frozen=True)
+class StagePlan:
+    stage: int
+    halfblocks: tuple[int, ...]   # hb = 2*layer (+1 for the MLP half)
+    embed: bool
+    head: bool
+
+
+def stage_partition(cfg: ModelConfig, num_stages: int) -> tuple[StagePlan, ...]:
+    """Contiguous split of the 2L half-blocks over ``num_stages`` stages.
+
+    Remainders go to the middle stages first (the end stages already carry
+    the embedding / LM head).  Every stage gets >= 0 half-blocks; stages
+    with none still pass activations through (and own embed/head if ends).
+    """
+    n = 2 * cfg.layers
+    base, rem = divmod(n, num_stages)
+    extra = [0] * num_stages
+    order = sorted(range(num_stages), key=lambda s: (abs(2 * s - (num_stages - 1)), s))
+    for s in order[:rem]:
+        extra[s] = 1
+    plans, start = [], 0
+    for s in range(num_stages):
+        cnt = base + extra[s]
+        plans.append(StagePlan(s, tuple(range(start, start + cnt)), s == 0, s == num_stages - 1))
+        start += cnt
+    assert start == n
+    return tuple(plans)
+
+
+def param_specs(cfg: ModelConfig):
+    """(name, shape, kind) for every parameter in a canonical order.
+    kind: 'w' (N(0,.02)), 'wo' (scaled output proj), 'b' (zero), 'g' (one)."""
+    h, f, V, S = cfg.hidden, cfg.ffn, cfg.vocab, cfg.seq
+    out = [("embed.wte", (V, h), "w"), ("embed.wpe", (S, h), "w")]
+    for l in range(cfg.layers):
+        p = f"layers.{l}."
+        out += [(p + "ln1.w", (h,), "g"), (p + "ln1.b", (h,), "b"),
+                (p + "attn.qkv.w", (3 * h, h), "w"), (p + "attn.qkv.b", (3 * h,), "b"),
+                (p + "attn.proj.w", (h, h), "wo"), (p + "attn.proj.b", (h,), "b"),
+                (p + "ln2.w", (h,), "g"), (p + "ln2.b", (h,), "b"),
+                (p + "mlp.fc1.w", (f, h), "w"), (p + "mlp.fc1.b", (f,), "b"),
+                (p + "mlp.fc2.w", (h, f), "wo"), (p + "mlp.fc2.b", (h,), "b")]
+    out += [("head.lnf.w", (h,), "g"), ("head.lnf.b", (h,), "b"), ("head.lm.w", (V, h), "w")]
+    return out
+
+
+def halfblock_param_names(hb: int) -> list[str]:
+    l, half = divmod(hb, 2)
+    p = f"layers.{l}."
+    if half == 0:
+        return [p + "ln1.w", p + "ln1.b", p + "attn.qkv.w", p + "attn.qkv.b", p + "attn.proj.w", p + "attn.proj.b"]
+    return [p + "ln2.w", p + "ln2.b", p + "mlp.fc1.w", p + "mlp.fc1.b", p + "mlp.fc2.w", p + "mlp.fc2.b"]
+
+
+def stage_param_names(plan: StagePlan) -> list[str]:
+    names = ["embed.wte", "embed.wpe"] if plan.embed else []
+    for hb in plan.halfblocks:
+        names += halfblock_param_names(hb)
+    if plan.head:
+        names += ["head.lnf.w", "head.lnf.b", "head.lm.w"]
+    return names
+
+
+def init_params(cfg: ModelConfig, seed: int = 1234, *, device="cpu", dtype=torch.float32,
+                perturb: bool = False) -> dict:
+    """Seeded initial parameters {name: tensor}; identical for every replica."""
+    gen = torch.Generator(device=device).manual_seed(seed)
+    out = {}
+    std = 0.02
+    std_o = 0.02 / math.sqrt(2 * cfg.layers)
+    for name, shape, kind in param_specs(cfg):
+        if kind in ("w", "wo"):
+            t = torch.randn(shape, generator=gen, device=device, dtype=torch.float32) * (std if kind == "w" else std_o)
+        elif kind == "b":
+            t = torch.zeros(shape, device=device, dtype=torch.float32)
+            if perturb:
+                t += 0.02 * torch.randn(shape, generator=gen, device=device, dtype=torch.float32)
+        else:
+            t = torch.ones(shape, device=device, dtype=torch.float32)
+            if perturb:
+                t += 0.05 * torch.randn(shape, generator=gen, device=device, dtype=torch.float32)
+        out[name] = t.to(dtype)
+    return out
+
+
+@dataclass
+class OptimConfig:
+    """AdamW hyper-parameters of the single post-flush update."""
+    lr: float = 1e-4
+    beta1: float = 0.9
+    beta2: float = 0.95
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+
+
+def synthetic_batch(cfg: ModelConfig, N: int, seed: int = 1234):
+    """i.i.d. uniform token ids [N, B, S] and targets (GPT: ids shifted by
+    one; BERT: independent random targets), from a seeded CPU generator
+    (SURVEY §8(d))."""
+    gen = torch.Generator().manual_seed(seed)
+    toks = torch.randint(0, cfg.vocab, (N, cfg.micro_batch, cfg.seq + 1), generator=gen, dtype=torch.int64)
+    if cfg.causal:
+        return toks[..., :-1].contiguous(), toks[..., 1:].contiguous()
+    tgt = torch.randint(0, cfg.vocab, (N, cfg.micro_batch, cfg.seq), generator=gen, dtype=torch.int64)
+    return toks[..., :-1].contiguous(), tgt

@@ -1,0 +1,226 @@
+"""Kernel-level numerics on the B200: every C-ABI kernel against a plain
+PyTorch fp32 reference of the same op (torch is only the checker here)."""
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2410_19367_b200.runtime import ops
+    from paper_2410_19367_b200.runtime.lib import EPI_DGELU, EPI_GELU, EPI_NONE
+
+
+def _gelu(x):
+    return 0.5 * x * (1 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+
+
+def _relerr(a, b):
+    a, b = a.double(), b.double()
+    return ((a - b).norm() / b.norm().clamp_min(1e-30)).item()
+
+
+@pytest.fixture(autouse=True)
+def _seed():
+    torch.manual_seed(0)
+
+
+SHAPES = [(128, 128, 64), (256, 512, 128), (300, 200, 192), (2048, 6144, 2048), (384, 2304, 1024),
+          (512, 50304 // 8, 256), (130, 136, 72)]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("ak,bk", [(True, True), (True, False), (False, False), (False, True)])
+def test_gemm_bf16_tc(M, N, K, ak, bk):
+    if (not ak and M % 8) or (not bk and N % 8) or K % 8:
+        pytest.skip("TMA needs 16-byte row pitches")
+    dev = "cuda"
+    A = torch.randn(M, K, device=dev) if ak else torch.randn(K, M, device=dev)
+    B = torch.randn(N, K, device=dev) if bk else torch.randn(K, N, device=dev)
+    A16, B16 = A.bfloat16(), B.bfloat16()
+    opA = A16.float() if ak else A16.float().t()
+    opB = B16.float().t() if bk else B16.float()
+    ref = opA @ opB
+    C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    ops.gemm(A16, B16, C, a_kmajor=ak, b_kmajor=bk)
+    torch.cuda.synchronize()
+    assert _relerr(C.float(), ref) < 1e-2
+    C32 = torch.randn(M, N, device=dev)
+    base = C32.clone()
+    ops.gemm(A16, B16, C32, a_kmajor=ak, b_kmajor=bk, beta=1.0, alpha=0.5)
+    torch.cuda.synchronize()
+    assert _relerr(C32, base + 0.5 * ref) < 2e-5 * math.sqrt(K) + 1e-4
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 512, 128), (300, 264, 96)])
+def test_gemm_epilogues(M, N, K):
+    dev = "cuda"
+    X = torch.randn(M, K, device=dev).bfloat16()
+    W = torch.randn(N, K, device=dev).bfloat16()
+    b = torch.randn(N, device=dev).bfloat16()
+    R = torch.randn(M, N, device=dev).bfloat16()
+    acc = X.float() @ W.float().t()
+    # bias + residual
+    C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    ops.gemm(X, W, C, bias=b, residual=R)
+    assert _relerr(C.float(), acc + b.float() + R.float()) < 1e-2
+    # bias + gelu (aux keeps pre-activation)
+    aux = torch.empty_like(C)
+    G = torch.empty_like(C)
+    ops.gemm(X, W, G, bias=b, aux=aux, epilogue=EPI_GELU)
+    pre = acc + b.float()
+    assert _relerr(aux.float(), pre) < 1e-2
+    assert _relerr(G.float(), _gelu(aux.float())) < 1e-2
+    # dgelu
+    D = torch.empty_like(C)
+    ops.gemm(X, W, D, aux=aux, epilogue=EPI_DGELU)
+    x = aux.float().requires_grad_(True)
+    _gelu(x).backward(torch.ones_like(x))
+    assert _relerr(D.float(), acc * x.grad) < 1e-2
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("ak,bk", [(True, True), (True, False), (False, False)])
+def test_gemm_fp32_simt_exact(ak, bk):
+    M, N, K = 97, 65, 33
+    A = torch.randn(M, K, device="cuda", dtype=torch.float64)
+    B = torch.randn(N, K, device="cuda", dtype=torch.float64)
+    ref = A @ B.t()
+    a = A.float() if ak else A.float().t().contiguous()
+    bb = B.float() if bk else B.float().t().contiguous()
+    C = torch.empty(M, N, device="cuda")
+    ops.gemm(a, bb, C, a_kmajor=ak, b_kmajor=bk)
+    torch.cuda.synchronize()
+    assert _relerr(C, ref) < 1e-6
+
+
+def test_gemm_tc_matches_simt_bitwise_close():
+    M, N, K = 512, 768, 512
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    B = torch.randn(N, K, device="cuda").bfloat16()
+    C1 = torch.empty(M, N, device="cuda")
+    C2 = torch.empty(M, N, device="cuda")
+    ops.gemm(A, B, C1)
+    ops.gemm(A, B, C2, force_simt=True)
+    torch.cuda.synchronize()
+    assert _relerr(C1, C2) < 1e-5
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("rows,cols", [(64, 64), (300, 1024), (2048, 2048), (17, 100)])
+def test_layernorm(dtype, rows, cols):
+    x = torch.randn(rows, cols, device="cuda").to(dtype)
+    g = (1 + 0.1 * torch.randn(cols, device="cuda")).to(dtype)
+    b = (0.1 * torch.randn(cols, device="cuda")).to(dtype)
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device="cuda")
+    rstd = torch.empty(rows, device="cuda")
+    ops.layernorm_fwd(x, g, b, y, mean, rstd, eps=1e-5)
+    xr = x.float().requires_grad_(True)
+    gr = g.float().requires_grad_(True)
+    br = b.float().requires_grad_(True)
+    yr = torch.nn.functional.layer_norm(xr, (cols,), gr, br, 1e-5)
+    tol = 1e-5 if dtype == torch.float32 else 1e-2
+    assert _relerr(y.float(), yr) < tol
+    dy = torch.randn_like(x)
+    dres = torch.randn_like(x)
+    yr.backward(dy.float())
+    dx = torch.empty_like(x)
+    dg = torch.zeros(cols, device="cuda")
+    db = torch.zeros(cols, device="cuda")
+    ops.layernorm_bwd(dy, x, g, mean, rstd, dx, dg, db, dres=dres)
+    torch.cuda.synchronize()
+    assert _relerr(dx.float(), xr.grad + dres.float()) < (1e-5 if dtype == torch.float32 else 2e-2)
+    assert _relerr(dg, gr.grad) < (1e-5 if dtype == torch.float32 else 2e-2)
+    assert _relerr(db, br.grad) < (1e-5 if dtype == torch.float32 else 2e-2)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_colsum_embed_xent_cast(dtype):
+    rows, cols = 777, 1000
+    x = torch.randn(rows, cols, device="cuda").to(dtype)
+    out = torch.ones(cols, device="cuda")
+    ops.colsum_acc(x, out)
+    assert _relerr(out, 1 + x.float().sum(0)) < 1e-5
+    B, S, H, V = 2, 64, 128, 500
+    tok = torch.randint(0, V, (B * S,), device="cuda", dtype=torch.int32)
+    wte = torch.randn(V, H, device="cuda").to(dtype)
+    wpe = torch.randn(S, H, device="cuda").to(dtype)
+    e = torch.empty(B * S, H, device="cuda", dtype=dtype)
+    ops.embed_fwd(tok, wte, wpe, e, B, S)
+    ref = wte.float()[tok.long()] + wpe.float().repeat(B, 1)
+    assert _relerr(e.float(), ref) < (1e-6 if dtype == torch.float32 else 1e-2)
+    dout = torch.randn(B * S, H, device="cuda").to(dtype)
+    dwte = torch.zeros(V, H, device="cuda")
+    dwpe = torch.zeros(S, H, device="cuda")
+    ops.embed_bwd(tok, dout, dwte, dwpe, B, S)
+    rwte = torch.zeros(V, H, device="cuda").index_add_(0, tok.long(), dout.float())
+    rwpe = dout.float().view(B, S, H).sum(0)
+    assert _relerr(dwte, rwte) < 1e-5 and _relerr(dwpe, rwpe) < 1e-5
+    logits = (3 * torch.randn(B * S, V, device="cuda")).to(dtype)
+    tgt = torch.randint(0, V, (B * S,), device="cuda", dtype=torch.int32)
+    lf = logits.float().requires_grad_(True)
+    lref = torch.nn.functional.cross_entropy(lf, tgt.long(), reduction="mean")
+    lref.backward()
+    loss = torch.zeros(1, device="cuda")
+    ops.xent_fwd_bwd(logits, tgt, loss, grad_scale=1.0 / (B * S), loss_scale=1.0 / (B * S))
+    torch.cuda.synchronize()
+    assert abs(loss.item() - lref.item()) / lref.item() < (1e-5 if dtype == torch.float32 else 1e-2)
+    assert _relerr(logits.float(), lf.grad) < (1e-4 if dtype == torch.float32 else 2e-2)
+    y = torch.empty(rows, cols, device="cuda", dtype=torch.float32)
+    ops.cast(x, y)
+    assert torch.equal(y, x.float())
+
+
+def _attn_ref(qkv, B, S, H, Dh, causal, scale):
+    q, k, v = qkv.float().view(B, S, 3, H, Dh).permute(2, 0, 3, 1, 4)
+    s = (q @ k.transpose(-1, -2)) * scale
+    if causal:
+        s = s.masked_fill(torch.triu(torch.ones(S, S, dtype=torch.bool, device=s.device), 1), float("-inf"))
+    p = s.softmax(-1)
+    o = (p @ v).permute(0, 2, 1, 3).reshape(B * S, H * Dh)
+    return o, torch.logsumexp(s, -1).reshape(-1)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("B,S,H,Dh,causal", [(2, 32, 4, 16, True), (1, 256, 2, 64, False), (1, 384, 2, 128, True),
+                                             (2, 128, 3, 64, True)])
+def test_attention(dtype, B, S, H, Dh, causal):
+    scale = 1.0 / math.sqrt(Dh)
+    qkv = torch.randn(B * S, 3 * H * Dh, device="cuda").to(dtype)
+    o = torch.empty(B * S, H * Dh, device="cuda", dtype=dtype)
+    lse = torch.empty(B * H * S, device="cuda")
+    ops.attn_fwd(qkv, o, lse, B, S, H, Dh, causal, scale)
+    x = qkv.float().requires_grad_(True)
+    oref, lref = _attn_ref(x, B, S, H, Dh, causal, scale)
+    tol = 1e-5 if dtype == torch.float32 else 2e-2
+    assert _relerr(o.float(), oref) < tol
+    assert _relerr(lse, lref) < 1e-3
+    dout = torch.randn_like(o)
+    oref.backward(dout.float())
+    dqkv = torch.empty_like(qkv)
+    ws = torch.empty(ops.attn_workspace_numel(B, S, H, Dh), device="cuda")
+    ops.attn_bwd(qkv, o, dout, lse, dqkv, ws, B, S, H, Dh, causal, scale)
+    torch.cuda.synchronize()
+    assert _relerr(dqkv.float(), x.grad) < (1e-4 if dtype == torch.float32 else 3e-2)
+
+
+def test_adam_matches_torch():
+    n = 1000003
+    p = torch.randn(n, device="cuda")
+    ga, gb = torch.randn(n, device="cuda"), torch.randn(n, device="cuda")
+    m, v = torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
+    master = p.clone()
+    pa = torch.empty(n, device="cuda", dtype=torch.bfloat16)
+    pb = torch.empty_like(pa)
+    tp = p.clone().requires_grad_(True)
+    opt = torch.optim.AdamW([tp], lr=1e-3, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1)
+    for step in (1, 2):
+        tp.grad = (ga + gb) * 0.5
+        opt.step()
+        ops.adam(master, ga, gb, m, v, pa, pb, lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1,
+                 step=step)
+    torch.cuda.synchronize()
+    assert _relerr(master, tp.detach()) < 1e-6
+    assert torch.equal(pa, pb) and torch.equal(pa, master.bfloat16())
