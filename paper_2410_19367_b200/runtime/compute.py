@@ -1,0 +1,177 @@
+"""One virtual stage's forward / backward pass as a sequence of C-ABI kernels.
+
+This is the body of the reference SPEC's per-task work ("each
+worker executes its task list in order; activations/gradients flow along
+schedule edges; gradients accumulate over micro-batches") for the
+transformer stages of ``model.py``.  Every launch goes to
+``libbitpipe_b200.so`` on the logical device's stream; torch only provides
+the buffers.
+
+Per half-block (x = residual stream, M = B*S tokens):
+  attn fwd : a=LN1(x) | qkv=a W^T+b (tcgen05) | o=attn(qkv) | x'=x+o Wo^T+bo
+             (bias + residual fused in the GEMM epilogue)
+  mlp  fwd : m=LN2(x) | g=gelu(m W1^T+b1), u saved (GELU epilogue) |
+             x'=x+g W2^T+b2
+  attn bwd : dWo+=dy^T o | dbo+=sum dy | do=dy Wo | dqkv=attn_bwd |
+             dWqkv+=dqkv^T a | dbqkv | da=dqkv Wqkv | dx=dy+LN1'(da)
+  mlp  bwd : dW2+=dy^T g | db2 | du=(dy W2)*gelu'(u) (dGELU epilogue) |
+             dW1+=du^T m | db1 | dm=du W1 | dx=dy+LN2'(dm)
+  head     : xf=LNf(x) | logits=xf Wlm^T | fused softmax-CE fwd+bwd in place
+             (loss to the micro-batch's slot) ; bwd: dxf=dlogits Wlm,
+             dWlm+=dlogits^T xf, dx=LNf'(dxf)
+  embed    : x0=wte[tok]+wpe ; bwd: scatter-add into dwte, dwpe
+Weight gradients accumulate in fp32 directly in the GEMM epilogue (beta=1).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from ..model import ModelConfig, StagePlan
+from . import ops
+from .lib import EPI_DGELU, EPI_GELU
+from .state import BufferPool, StageParams
+
+__all__ = ["Stash", "StageCompute"]
+
+
+@dataclass
+class Stash:
+    xs: list                      # residual stream: xs[0] = stage input
+    saves: list = field(default_factory=list)
+    head: tuple | None = None
+    tokens: torch.Tensor | None = None
+
+    def buffers(self):
+        out = list(self.xs)
+        for s in self.saves:
+            out.extend(s[1:])
+        if self.head is not None:
+            out.extend(self.head)
+        return out
+
+
+class StageCompute:
+    """Forward/backward of one stage replica with a fixed parameter store."""
+
+    def __init__(self, cfg: ModelConfig, plan: StagePlan, params: StageParams, *, grad_scale: float):
+        self.cfg, self.plan, self.sp = cfg, plan, params
+        self.dtype = params.dtype
+        self.M = cfg.micro_batch * cfg.seq
+        self.grad_scale = grad_scale          # d(step objective)/d(micro-batch mean loss)
+        self.loss_scale = 1.0 / self.M
+
+    # ------------------------------------------------------------- forward --
+    def forward(self, stream, pool: BufferPool, *, x0=None, tokens=None, targets=None, loss_slot=None):
+        cfg, P = self.cfg, self.sp.p
+        M, h, dt = self.M, cfg.hidden, self.dtype
+        f32 = torch.float32
+        if self.plan.embed:
+            x0 = pool.get((M, h), dt, stream)
+            ops.embed_fwd(tokens, P["embed.wte"], P["embed.wpe"], x0, cfg.micro_batch, cfg.seq, stream=stream)
+        st = Stash(xs=[x0], tokens=tokens)
+        H, Dh = cfg.heads, cfg.head_dim
+        scale = 1.0 / math.sqrt(Dh)
+        for hb in self.plan.halfblocks:
+            l, half = divmod(hb, 2)
+            p = f"layers.{l}."
+            x = st.xs[-1]
+            mean, rstd = pool.get((M,), f32, stream), pool.get((M,), f32, stream)
+            y = pool.get((M, h), dt, stream)
+            if half == 0:
+                a = pool.get((M, h), dt, stream)
+                ops.layernorm_fwd(x, P[p + "ln1.w"], P[p + "ln1.b"], a, mean, rstd, cfg.ln_eps, stream=stream)
+                qkv = pool.get((M, 3 * h), dt, stream)
+                ops.gemm(a, P[p + "attn.qkv.w"], qkv, bias=P[p + "attn.qkv.b"], stream=stream)
+                o = pool.get((M, h), dt, stream)
+                lse = pool.get((cfg.micro_batch * H * cfg.seq,), f32, stream)
+                ops.attn_fwd(qkv, o, lse, cfg.micro_batch, cfg.seq, H, Dh, cfg.causal, scale, stream=stream)
+                ops.gemm(o, P[p + "attn.proj.w"], y, bias=P[p + "attn.proj.b"], residual=x, stream=stream)
+                st.saves.append(("attn", a, mean, rstd, qkv, o, lse))
+            else:
+                m = pool.get((M, h), dt, stream)
+                ops.layernorm_fwd(x, P[p + "ln2.w"], P[p + "ln2.b"], m, mean, rstd, cfg.ln_eps, stream=stream)
+                u = pool.get((M, cfg.ffn), dt, stream)
+                g = pool.get((M, cfg.ffn), dt, stream)
+                ops.gemm(m, P[p + "mlp.fc1.w"], g, bias=P[p + "mlp.fc1.b"], aux=u, epilogue=EPI_GELU, stream=stream)
+                ops.gemm(g, P[p + "mlp.fc2.w"], y, bias=P[p + "mlp.fc2.b"], residual=x, stream=stream)
+                st.saves.append(("mlp", m, mean, rstd, u, g))
+            st.xs.append(y)
+        if self.plan.head:
+            x = st.xs[-1]
+            xf = pool.get((M, h), dt, stream)
+            mean, rstd = pool.get((M,), f32, stream), pool.get((M,), f32, stream)
+            ops.layernorm_fwd(x, P["head.lnf.w"], P["head.lnf.b"], xf, mean, rstd, cfg.ln_eps, stream=stream)
+            logits = pool.get((M, cfg.vocab), dt, stream)
+            ops.gemm(xf, P["head.lm.w"], logits, stream=stream)
+            ops.xent_fwd_bwd(logits, targets, loss_slot, grad_scale=self.grad_scale * self.loss_scale,
+                             loss_scale=self.loss_scale, stream=stream)
+            st.head = (xf, mean, rstd, logits)
+            return st, None
+        out = st.xs.pop()          # ownership moves to the consumer of the message
+        return st, out
+
+    # ------------------------------------------------------------ backward --
+    def backward(self, stream, pool: BufferPool, st: Stash, dy, ws):
+        """Returns (dx0 or None, buffers to release after this task)."""
+        cfg, P, G = self.cfg, self.sp.p, self.sp.g
+        M, h, dt = self.M, cfg.hidden, self.dtype
+        H, Dh = cfg.heads, cfg.head_dim
+        scale = 1.0 / math.sqrt(Dh)
+        release = st.buffers()
+        if self.plan.head:
+            xf, mean, rstd, dlogits = st.head
+            dxf = pool.get((M, h), dt, stream)
+            ops.gemm(dlogits, P["head.lm.w"], dxf, b_kmajor=False, stream=stream)
+            ops.gemm(dlogits, xf, G["head.lm.w"], a_kmajor=False, b_kmajor=False, beta=1.0, stream=stream)
+            dy = pool.get((M, h), dt, stream)
+            ops.layernorm_bwd(dxf, st.xs[-1], P["head.lnf.w"], mean, rstd, dy, G["head.lnf.w"], G["head.lnf.b"],
+                              stream=stream)
+            release += [dxf, dy]
+        else:
+            release.append(dy)
+        for i in range(len(self.plan.halfblocks) - 1, -1, -1):
+            l, half = divmod(self.plan.halfblocks[i], 2)
+            p = f"layers.{l}."
+            x = st.xs[i]
+            save = st.saves[i]
+            dx = pool.get((M, h), dt, stream)
+            if half == 0:
+                _, a, mean, rstd, qkv, o, lse = save
+                ops.gemm(dy, o, G[p + "attn.proj.w"], a_kmajor=False, b_kmajor=False, beta=1.0, stream=stream)
+                ops.colsum_acc(dy, G[p + "attn.proj.b"], stream=stream)
+                do = pool.get((M, h), dt, stream)
+                ops.gemm(dy, P[p + "attn.proj.w"], do, b_kmajor=False, stream=stream)
+                dqkv = pool.get((M, 3 * h), dt, stream)
+                ops.attn_bwd(qkv, o, do, lse, dqkv, ws, cfg.micro_batch, cfg.seq, H, Dh, cfg.causal, scale,
+                             stream=stream)
+                ops.gemm(dqkv, a, G[p + "attn.qkv.w"], a_kmajor=False, b_kmajor=False, beta=1.0, stream=stream)
+                ops.colsum_acc(dqkv, G[p + "attn.qkv.b"], stream=stream)
+                da = pool.get((M, h), dt, stream)
+                ops.gemm(dqkv, P[p + "attn.qkv.w"], da, b_kmajor=False, stream=stream)
+                ops.layernorm_bwd(da, x, P[p + "ln1.w"], mean, rstd, dx, G[p + "ln1.w"], G[p + "ln1.b"], dres=dy,
+                                  stream=stream)
+                release += [do, dqkv, da]
+            else:
+                _, m, mean, rstd, u, g = save
+                ops.gemm(dy, g, G[p + "mlp.fc2.w"], a_kmajor=False, b_kmajor=False, beta=1.0, stream=stream)
+                ops.colsum_acc(dy, G[p + "mlp.fc2.b"], stream=stream)
+                du = pool.get((M, cfg.ffn), dt, stream)
+                ops.gemm(dy, P[p + "mlp.fc2.w"], du, b_kmajor=False, aux=u, epilogue=EPI_DGELU, stream=stream)
+                ops.gemm(du, m, G[p + "mlp.fc1.w"], a_kmajor=False, b_kmajor=False, beta=1.0, stream=stream)
+                ops.colsum_acc(du, G[p + "mlp.fc1.b"], stream=stream)
+                dm = pool.get((M, h), dt, stream)
+                ops.gemm(du, P[p + "mlp.fc1.w"], dm, b_kmajor=False, stream=stream)
+                ops.layernorm_bwd(dm, x, P[p + "ln2.w"], mean, rstd, dx, G[p + "ln2.w"], G[p + "ln2.b"], dres=dy,
+                                  stream=stream)
+                release += [du, dm]
+            if i > 0 or self.plan.embed:
+                release.append(dx)
+            dy = dx
+        if self.plan.embed:
+            ops.embed_bwd(st.tokens, dy, G["embed.wte"], G["embed.wpe"], cfg.micro_batch, cfg.seq, stream=stream)
+            return None, release
+        # dy is now the gradient w.r.t. the stage input: it becomes the message
+        return dy, [t for t in release if t is not dy]

@@ -1,0 +1,309 @@
+"""The BitPipe train step: executes a :class:`Schedule` on CUDA streams.
+
+This is the B200 realisation of the reference SPEC's absent ``runtime``
+module (``run_schedule_numeric``) for the transformer model
+of :mod:`..model`:
+
+* every logical device ``d`` of the schedule gets its own CUDA stream and
+  runs ``schedule.per_device[d]`` strictly in list order (the order is the
+  bit-exact reference order);
+* activation / gradient messages are tag-addressed by (kind, direction,
+  micro-batch, destination stage) -- never by arrival order -- because the
+  reference orders are not FIFO-consistent per link;
+* eager gradient synchronisation: as soon as a stage's last backward on a
+  device is issued, that stage's replica-pair gradient mean and AdamW update
+  are issued on the optimizer stream, overlapping the rest of the drain
+  (PAPER.md:151-153);
+* one weight update per iteration, after all uses of the stage's weights.
+
+Placement modes
+  coresident  (one process, one GPU): all D logical devices share the GPU,
+              each on its own stream; messages are zero-copy hand-offs gated
+              by CUDA events; the replica-pair "allreduce" is the fused
+              (g_down + g_up)/2 read inside the Adam kernel.
+  distributed (one process per GPU, world == D, rank == logical device):
+              messages move over NCCL P2P (torch.distributed) with receives
+              posted up-front in the sender's order on one group per link
+              direction; the pair mean is a 2-rank NCCL all-reduce on a
+              per-(pair, stage) group, followed by the local Adam.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import torch
+
+from ..model import CONFIGS, ModelConfig, OptimConfig, stage_partition
+from ..schedule import Direction, Schedule, TaskKind, canonical_replay
+from . import ops
+from .compute import StageCompute
+from .state import BufferPool, StageParams
+
+__all__ = ["Trainer", "StepOutput", "issue_order"]
+
+
+@dataclass
+class StepOutput:
+    losses: torch.Tensor           # [N] fp32 device tensor, index = micro-batch id - 1
+    step: int
+    task_events: dict | None = None
+
+
+def issue_order(schedule: Schedule):
+    """A single-thread issue order over all (device, position) pairs that is a
+    topological order of dataflow + per-device order: sort by the canonical
+    ASAP start time (dependencies end no later than a task starts and have
+    positive duration), ties by device then position."""
+    starts, _ = canonical_replay(schedule)
+    items = []
+    for d, row in enumerate(schedule.per_device):
+        for i, t in enumerate(row):
+            items.append((starts[t], d, i, t))
+    items.sort(key=lambda x: (x[0], x[1], x[2]))
+    return [(d, i, t) for _, d, i, t in items]
+
+
+class Trainer:
+    """Executes BitPipe (or any schedule from :mod:`..schedule`) on one GPU
+    (coresident) or one process per logical device (distributed).
+
+    ``train_step(tokens, targets)`` runs one iteration: N micro-batches
+    through the schedule, eager replica-pair gradient sync, one AdamW update.
+    """
+
+    def __init__(self, cfg: ModelConfig, schedule: Schedule, *, dtype=torch.bfloat16, optim: OptimConfig | None = None,
+                 params: dict | None = None, seed: int = 1234, device=None, dist_ctx=None, record_timeline=False):
+        if not torch.cuda.is_available():
+            raise RuntimeError("BitPipe Trainer needs a CUDA device (no CPU fallback)")
+        ops.lib()  # fail loudly now if the kernel library is missing
+        self.cfg, self.sched = cfg, schedule
+        self.dtype = dtype
+        self.optim = optim or OptimConfig()
+        self.D, self.v = schedule.D, schedule.v
+        self.S = schedule.num_stages
+        self.N = schedule.N
+        self.dirs = list(schedule.directions)
+        self.bidir = len(self.dirs) == 2
+        self.n_rep = self.N // len(self.dirs)
+        self.plans = stage_partition(cfg, self.S)
+        self.dist = dist_ctx
+        self.device = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
+        torch.cuda.set_device(self.device)
+        self.local_devices = list(range(self.D)) if dist_ctx is None else [dist_ctx.rank]
+        self.record_timeline = record_timeline
+        self.step_count = 0
+
+        # -- parameters: one StageParams per (direction, stage) held locally --
+        if params is None:
+            from ..model import init_params
+            params = init_params(cfg, seed, device=self.device)
+        self.stage_params: dict = {}
+        self.compute: dict = {}
+        grad_scale = 1.0 / self.n_rep
+        for dr in self.dirs:
+            smap = schedule.stage_map(dr)
+            for s in range(self.S):
+                if smap.device_of(s) not in self.local_devices:
+                    continue
+                sp = StageParams(cfg, self.plans[s], dtype, self.device)
+                sp.load(params)
+                self.stage_params[(dr, s)] = sp
+                self.compute[(dr, s)] = StageCompute(cfg, self.plans[s], sp, grad_scale=grad_scale)
+        # optimizer state: one master/m/v per stage present locally (coresident:
+        # shared by the two replicas; distributed: per local replica)
+        self.opt_owner: dict = {}
+        for (dr, s), sp in self.stage_params.items():
+            key = s if dist_ctx is None else (dr, s)
+            if key not in self.opt_owner:
+                sp.init_optimizer(params)
+                self.opt_owner[key] = sp
+        del params
+
+        # -- streams, pools, workspaces ------------------------------------------------
+        self.streams = {d: torch.cuda.Stream(device=self.device) for d in self.local_devices}
+        self.opt_stream = torch.cuda.Stream(device=self.device)
+        self.pool = BufferPool(self.device)
+        wsn = ops.attn_workspace_numel(cfg.micro_batch, cfg.seq, cfg.heads, cfg.head_dim)
+        self.ws = {d: torch.empty(wsn, dtype=torch.float32, device=self.device) for d in self.local_devices}
+        self.losses = torch.zeros(self.N, dtype=torch.float32, device=self.device)
+        self.last_b = schedule.last_backward_positions()
+        if dist_ctx is None:
+            self.order = issue_order(schedule)
+        else:
+            d = dist_ctx.rank
+            self.order = [(d, i, t) for i, t in enumerate(schedule.per_device[d])]
+            dist_ctx.setup(self)
+        self.iter_done = None
+        self.timeline = None
+
+    # ----------------------------------------------------------------- helpers --
+    def _dev_of(self, dr: Direction, s: int) -> int:
+        return self.sched.stage_map(dr).device_of(s)
+
+    def _zero_grads(self):
+        for (dr, s), sp in self.stage_params.items():
+            st = self.streams[self._dev_of(dr, s)]
+            with torch.cuda.stream(st):
+                sp.grad.zero_()
+
+    def _adam(self, stage_key, grads, params_out, stream):
+        owner = self.opt_owner[stage_key]
+        o = self.optim
+        ops.adam(owner.master, grads[0], grads[1] if len(grads) > 1 else None, owner.m, owner.v,
+                 params_out[0], params_out[1] if len(params_out) > 1 else None,
+                 lr=o.lr, beta1=o.beta1, beta2=o.beta2, eps=o.eps, weight_decay=o.weight_decay,
+                 step=self.step_count, stream=stream)
+
+    # --------------------------------------------------------------- train step --
+    def train_step(self, tokens: torch.Tensor, targets: torch.Tensor) -> StepOutput:
+        """tokens/targets: int32 device tensors [N, B, S] already on this GPU."""
+        cfg = self.cfg
+        self.step_count += 1
+        main = torch.cuda.current_stream(self.device)
+        start_ev = torch.cuda.Event()
+        if self.iter_done is not None:
+            main.wait_event(self.iter_done)
+        self.losses.zero_()
+        start_ev.record(main)
+        for st in self.streams.values():
+            st.wait_event(start_ev)
+        self.opt_stream.wait_event(start_ev)
+        self._zero_grads()
+        if self.dist is not None:
+            self.dist.begin_iteration(self)
+
+        msgs: dict = {}
+        stashes: dict = {}
+        done_dirs: dict = {}
+        tl = [] if self.record_timeline else None
+        M = cfg.micro_batch * cfg.seq
+        for d, i, t in self.order:
+            stream = self.streams[d]
+            dr, s, mb = t.direction, t.stage, t.micro_batch
+            comp = self.compute[(dr, s)]
+            if tl is not None:
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev0.record(stream)
+            if t.kind is TaskKind.FORWARD:
+                x0 = None
+                if s > 0:
+                    x0 = self._recv(msgs, ("act", dr, mb, s), d)
+                tok = tokens[mb - 1].reshape(-1)
+                tgt = targets[mb - 1].reshape(-1)
+                stash, out = comp.forward(stream, self.pool, x0=x0, tokens=tok, targets=tgt,
+                                          loss_slot=self.losses[mb - 1:mb])
+                stashes[(dr, mb, s)] = stash
+                if out is not None:
+                    self._send(msgs, ("act", dr, mb, s + 1), out, d, self._dev_of(dr, s + 1))
+            else:
+                dy = None
+                if s < self.S - 1:
+                    dy = self._recv(msgs, ("grad", dr, mb, s), d)
+                stash = stashes.pop((dr, mb, s))
+                dx, release = comp.backward(stream, self.pool, stash, dy, self.ws[d])
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                self.pool.put_all(release, ev)
+                if dx is not None:
+                    self._send(msgs, ("grad", dr, mb, s - 1), dx, d, self._dev_of(dr, s - 1), event=ev)
+                if self.last_b[d].get((dr, s)) == i:
+                    self._stage_grads_ready(dr, s, d, ev, done_dirs)
+            if tl is not None:
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev1.record(stream)
+                tl.append((d, i, t, ev0, ev1))
+        if stashes or (msgs and self.dist is None):
+            raise RuntimeError(f"protocol violation: {len(stashes)} stashes / {len(msgs)} messages left at flush")
+        if self.dist is not None:
+            self.dist.end_iteration(self)
+        done = torch.cuda.Event()
+        done.record(self.opt_stream)
+        for st in self.streams.values():
+            ev = torch.cuda.Event()
+            ev.record(st)
+            main.wait_event(ev)
+        main.wait_event(done)
+        self.iter_done = torch.cuda.Event()
+        self.iter_done.record(main)
+        self.timeline = tl
+        return StepOutput(self.losses, self.step_count)
+
+    # ---------------------------------------------------------------- messages --
+    def _send(self, msgs, key, tensor, src, dst, event=None):
+        if self.dist is not None and dst != src:
+            self.dist.send(self, key, tensor, src, dst)
+            return
+        if event is None:
+            event = torch.cuda.Event()
+            event.record(self.streams[src])
+        msgs[key] = (tensor, event)
+
+    def _recv(self, msgs, key, d):
+        item = msgs.pop(key, None)
+        if item is None:
+            if self.dist is not None:
+                return self.dist.recv(self, key, d)
+            raise RuntimeError(f"protocol violation: task on device {d} needs {key} which was never produced")
+        tensor, ev = item
+        self.streams[d].wait_event(ev)
+        return tensor
+
+    # ----------------------------------------------------------- eager sync --
+    def _stage_grads_ready(self, dr, s, d, ev, done_dirs):
+        if self.dist is not None:
+            self.dist.sync_stage(self, dr, s, ev)
+            return
+        done_dirs.setdefault(s, {})[dr] = ev
+        if len(done_dirs[s]) < len(self.dirs):
+            return
+        st = self.opt_stream
+        for e in done_dirs[s].values():
+            st.wait_event(e)
+        grads = [self.stage_params[(x, s)].grad for x in self.dirs]
+        outs = [self.stage_params[(x, s)].flat for x in self.dirs]
+        self._adam(s, grads, outs, st)
+
+    # ---------------------------------------------------------- introspection --
+    def gather(self, what: str = "params", direction: Direction | None = None) -> dict:
+        """{name: fp32 CPU tensor} of the local replica's params / grads /
+        master weights (tests only; synchronises)."""
+        torch.cuda.synchronize(self.device)
+        out = {}
+        dirs = [direction] if direction is not None else self.dirs
+        for (dr, s), sp in self.stage_params.items():
+            if dr not in dirs:
+                continue
+            for n in sp.names:
+                if what == "params":
+                    t = sp.p[n]
+                elif what == "grads":
+                    t = sp.g[n]
+                elif what == "master":
+                    owner = self.opt_owner[s if self.dist is None else (dr, s)]
+                    t = owner.master_view(n)
+                else:
+                    raise ValueError(what)
+                out.setdefault(n, t.detach().float().cpu().clone())
+        return out
+
+    def measured_bubble(self):
+        """Per-device busy time / makespan from the last step's per-task CUDA
+        events and beta = 1 - sum busy / (D * makespan).
+
+        Meaningful in distributed mode (one GPU per logical device); in
+        coresident mode the D streams share one GPU and the number only
+        describes stream occupancy."""
+        if not self.timeline:
+            return None
+        torch.cuda.synchronize(self.device)
+        first = self.timeline[0][3]
+        spans: dict = {}
+        for d, i, t, e0, e1 in self.timeline:
+            spans.setdefault(d, []).append((first.elapsed_time(e0), first.elapsed_time(e1)))
+        busy = {d: sum(b - a for a, b in v) for d, v in spans.items()}
+        start = min(a for v in spans.values() for a, _ in v)
+        end = max(b for v in spans.values() for _, b in v)
+        mk = end - start
+        beta = 1 - sum(busy.values()) / (len(spans) * mk) if mk > 0 else 0.0
+        return {"busy_ms": busy, "makespan_ms": mk, "bubble": beta}

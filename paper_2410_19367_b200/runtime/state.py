@@ -1,0 +1,100 @@
+"""Per-stage parameter / gradient / optimizer storage and the buffer pool.
+
+HBM layout: every (direction replica, virtual stage) owns one
+flat parameter buffer in the compute dtype plus one flat fp32 gradient
+buffer with identical offsets (64-element aligned, so every tensor view is
+16-byte aligned for the vectorised kernels and TMA).  The AdamW master
+weights and moments are flat fp32 buffers owned by the process that runs
+that stage's update.  Flat buffers make the eager replica-pair gradient
+sync one contiguous collective (or one fused kernel) per stage.
+"""
+from __future__ import annotations
+
+import math
+from collections import defaultdict
+
+import torch
+
+from ..model import ModelConfig, StagePlan, param_specs, stage_param_names
+
+__all__ = ["StageParams", "BufferPool", "ALIGN"]
+
+ALIGN = 64
+
+
+class StageParams:
+    """Flat storage of one stage replica's parameters and gradients."""
+
+    def __init__(self, cfg: ModelConfig, plan: StagePlan, dtype: torch.dtype, device):
+        shapes = {n: s for n, s, _ in param_specs(cfg)}
+        self.names = stage_param_names(plan)
+        self.offsets = {}
+        off = 0
+        for n in self.names:
+            self.offsets[n] = off
+            off += -(-math.prod(shapes[n]) // ALIGN) * ALIGN
+        self.numel = max(off, ALIGN)
+        self.dtype = dtype
+        self.device = torch.device(device)
+        self.flat = torch.zeros(self.numel, dtype=dtype, device=device)
+        self.grad = torch.zeros(self.numel, dtype=torch.float32, device=device)
+        self.shapes = {n: tuple(shapes[n]) for n in self.names}
+        self.p = {n: self._view(self.flat, n) for n in self.names}
+        self.g = {n: self._view(self.grad, n) for n in self.names}
+        self.master = self.m = self.v = None
+
+    def _view(self, flat, n):
+        o = self.offsets[n]
+        return flat[o:o + math.prod(self.shapes[n])].view(self.shapes[n])
+
+    def load(self, params: dict) -> None:
+        for n in self.names:
+            self.p[n].copy_(params[n].to(device=self.device, dtype=self.dtype))
+
+    def init_optimizer(self, params: dict | None = None) -> None:
+        """Allocate fp32 master/m/v; master from ``params`` (exact fp32) when
+        given, else from the working copy."""
+        self.master = torch.zeros(self.numel, dtype=torch.float32, device=self.device)
+        self.m = torch.zeros_like(self.master)
+        self.v = torch.zeros_like(self.master)
+        for n in self.names:
+            o = self.offsets[n]
+            src = params[n] if params is not None else self.p[n]
+            self.master[o:o + src.numel()].copy_(src.reshape(-1).to(device=self.device, dtype=torch.float32))
+
+    def master_view(self, n):
+        return self._view(self.master, n)
+
+
+class BufferPool:
+    """Event-guarded free lists of device buffers keyed by (shape, dtype).
+
+    ``get`` hands out a free buffer after making the requesting stream wait
+    for the event recorded when it was released (so reuse across the
+    per-logical-device streams is ordered); ``put_all`` releases a batch of
+    buffers under one event.  After the first iteration every request is a
+    hit, so the steady state allocates nothing.
+    """
+
+    def __init__(self, device):
+        self.device = torch.device(device)
+        self.free = defaultdict(list)
+        self.allocated_bytes = 0
+
+    def get(self, shape, dtype, stream):
+        key = (tuple(shape), dtype)
+        lst = self.free[key]
+        if lst:
+            t, ev = lst.pop()
+            if ev is not None:
+                stream.wait_event(ev)
+            return t
+        with torch.cuda.stream(stream):
+            t = torch.empty(key[0], dtype=dtype, device=self.device)
+        self.allocated_bytes += t.numel() * t.element_size()
+        return t
+
+    def put_all(self, tensors, event) -> None:
+        for t in tensors:
+            if t is not None:
+                self.free[(tuple(t.shape), t.dtype)].append((t, event))

@@ -60,7 +60,24 @@ def sweep_specs():
 
 
 def label(spec: dict) -> str:
-    return ",".join(f"{k}={spec[k]}" for k in sorted(spec))
+    """Stable text key, e.g. ``D=4;N=8;approach=bitpipe;policy=unit-1f1b:0:3;v=2``."""
+    def fmt(k, x):
+        return ":".join(str(int(e)) if isinstance(e, bool) else str(e) for e in x) if k == "policy" else str(x)
+    return ";".join(f"{k}={fmt(k, spec[k])}" for k in sorted(spec))
+
+
+def parse_label(text: str) -> dict:
+    spec = {}
+    for kv in text.split(";"):
+        k, x = kv.split("=", 1)
+        if k == "policy":
+            pri, defer, g = x.split(":")
+            spec[k] = [pri, bool(int(defer)), int(g)]
+        elif k == "approach":
+            spec[k] = x
+        else:
+            spec[k] = int(x)
+    return spec
 
 
 def run_ref(spec: dict):
