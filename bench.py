@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""BitPipe train-step benchmark (one JSON line on rank 0).
+
+Workload (BASELINE.json metric "GPT tokens/sec/box ... (frac of roofline);
+bubble fraction"): GPT-1.3B (24 layers, h=2048, s=2048, V=50304, B=1),
+BitPipe v=2, N=16 micro-batches per iteration (global batch 16 x 2048
+tokens), bf16 compute with fp32 master weights / AdamW.
+
+  --gpus 1 : the flagship D=8 schedule with all 8 logical devices
+             co-resident on GPU 0 (one CUDA stream each).
+  --gpus n : one process per GPU (torchrun), D = n logical devices, same
+             N = 16 micro-batches -> fixed total work ("strong" scaling).
+
+``value`` is tokens/s with inputs already in HBM; ``e2e`` is the same step
+through the public ``Trainer.train_step`` API with the tokens copied from
+pinned host memory and the per-micro-batch losses read back every step.
+``--impl reference`` times the CPU restatement of the train step (the
+reference has no numeric implementation) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GPT tokens/sec/box at D=1/2/4/8 B200 (frac of roofline); bubble fraction"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="gpt-1.3b")
+    ap.add_argument("--approach", default="bitpipe")
+    ap.add_argument("--D", type=int, default=None)
+    ap.add_argument("--N", type=int, default=16)
+    ap.add_argument("--paper-policy", action="store_true",
+                    help="use the F2 LayoutPolicy order that reaches the analytic bubble")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), p["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            with open(self.path) as f:
+                for line in f:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) >= 9:
+                        rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def reference_arm(args):
+    """CPU restatement of the train step (oracle), bounded sample per step."""
+    import torch
+    from oracle.gpt_oracle import OracleConfig, layer_sample_seconds
+    from paper_2410_19367_b200.model import CONFIGS, flops_per_token
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    oc = OracleConfig(cfg.layers, cfg.hidden, cfg.heads, cfg.seq, cfg.vocab, cfg.micro_batch, cfg.causal)
+    M = cfg.micro_batch * cfg.seq
+    layer_flops = 3.0 * (24 * cfg.hidden ** 2 + 4 * cfg.seq * cfg.hidden) * M
+    scale = flops_per_token(cfg) * M / layer_flops  # sample -> one micro-batch through the whole model
+    for _ in range(max(1, min(args.warmup, 1))):
+        layer_sample_seconds(oc)
+    times = [layer_sample_seconds(oc) for _ in range(max(1, args.steps))]
+    t = statistics.median(times)
+    value = M / (t * scale)
+    D = args.D or 8
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": len(times), "warmup": 1, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name} {args.approach} D={D} N={args.N} (CPU sample)",
+                   "global_batch": args.N * cfg.micro_batch, "seq_len": cfg.seq},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "sample": f"fwd+bwd of 1 transformer layer on 1 micro-batch ({M} tokens), fp32 torch CPU, "
+                                   f"extrapolated by model FLOPs (x{scale:.1f}) to whole-model tokens/s"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2410_19367_b200 import schedule as ps
+    from paper_2410_19367_b200.model import CONFIGS, OptimConfig, flops_per_token, synthetic_batch
+    from paper_2410_19367_b200.runtime import ops
+    from paper_2410_19367_b200.runtime.executor import Trainer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    cfg = CONFIGS[args.config]
+    dist_ctx = None
+    if world > 1:
+        from paper_2410_19367_b200.runtime.distributed import DistContext
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        D = world
+        dist_ctx = DistContext(rank, world)
+    else:
+        D = args.D or 8
+    N = args.N
+    approach = ps.ApproachId.parse(args.approach)
+    policy = ps.paper_policy(D) if args.paper_policy else None
+    if approach in (ps.ApproachId.BITPIPE, ps.ApproachId.BITPIPE_EARLY_FORWARD):
+        sched = ps.build_bitpipe(D, N, 2, approach is ps.ApproachId.BITPIPE_EARLY_FORWARD, policy=policy)
+    else:
+        sched = ps.build(approach, D, N)
+    tr = Trainer(cfg, sched, dtype=torch.bfloat16, optim=OptimConfig(), dist_ctx=dist_ctx)
+    tok, tgt = synthetic_batch(cfg, N, seed=1234)
+    tok_h = tok.int().pin_memory()
+    tgt_h = tgt.int().pin_memory()
+    tok_d, tgt_d = tok_h.cuda(), tgt_h.cuda()
+    main_stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        tr.train_step(tok_d, tgt_d)
+    barrier()
+    launches0 = ops.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(main_stream)
+        for _ in range(args.steps):
+            out = tr.train_step(tok_d, tgt_d)
+        ev1.record(main_stream)
+        barrier()
+    launches = ops.launch_count() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    tokens_per_step = N * cfg.micro_batch * cfg.seq
+    value = tokens_per_step / (ms / 1e3)
+    loss_mean = out.losses.float().mean().item()
+
+    # ---- end to end through the public API: H2D inputs + D2H losses per step
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        t0 = time.perf_counter()
+        e2e_steps = max(3, args.steps // 2)
+        for _ in range(e2e_steps):
+            td = tok_h.to("cuda", non_blocking=True)
+            gd = tgt_h.to("cuda", non_blocking=True)
+            o = tr.train_step(td, gd)
+            host_losses = o.losses.to("cpu")
+        barrier()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = t.item()
+        e2e = {"value": tokens_per_step / (e2e_ms / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": tok_h.numel() * 4 + tgt_h.numel() * 4,
+               "d2h_bytes_per_step": host_losses.numel() * 4, "ms_per_step": e2e_ms}
+
+    # ---- roofline: whole step and the dominant kernel (tcgen05 GEMM)
+    peak_burst, peak_sust, hbm, peak_kind = _peaks()
+    F_tok = flops_per_token(cfg)
+    G = max(world, 1)
+    beta_ideal = float(ps.analytic_bubble_ratio(approach, D, N)) if G > 1 else 0.0
+    roof_tps = G * peak_sust * 1e12 * (1 - beta_ideal) / F_tok
+    beta_order = float(ps.canonical_bubble(sched))
+    # dominant kernel: MLP fc1 forward GEMM of one micro-batch (M=B*S, N=4h, K=h), timed live
+    Mtok = cfg.micro_batch * cfg.seq
+    A = torch.randn(Mtok, cfg.hidden, device="cuda").bfloat16()
+    W = torch.randn(cfg.ffn, cfg.hidden, device="cuda").bfloat16()
+    C = torch.empty(Mtok, cfg.ffn, device="cuda", dtype=torch.bfloat16)
+    for _ in range(5):
+        ops.gemm(A, W, C)
+    torch.cuda.synchronize()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 50
+    k0.record(main_stream)
+    for _ in range(reps):
+        ops.gemm(A, W, C)
+    k1.record(main_stream)
+    torch.cuda.synchronize()
+    gemm_ms = k0.elapsed_time(k1) / reps
+    gemm_flops = 2.0 * Mtok * cfg.ffn * cfg.hidden
+    achieved = gemm_flops / (gemm_ms / 1e3) / 1e12
+    del A, W, C
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": G, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform token ids, seed 1234; random-init "
+                                                            "weights N(0,0.02))",
+            "config": {"workload": f"{cfg.name} {approach.value} v=2 D={D} N={N}"
+                                   + (" (F2 paper policy)" if policy else "")
+                                   + (" all logical devices co-resident on 1 GPU" if G == 1 else ""),
+                       "global_batch": N * cfg.micro_batch, "seq_len": cfg.seq, "layers": cfg.layers,
+                       "hidden": cfg.hidden, "vocab": cfg.vocab, "parallelism": f"pp{D} bidirectional",
+                       "l2": "working set (2.6 GB weights, GBs of activations) >> 126 MB L2"},
+            "loss_mean": loss_mean,
+            "e2e": e2e,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s",
+                         "frac": achieved / peak_burst, "traffic": None,
+                         "kernel": f"bp gemm_tc fc1 fprop {Mtok}x{cfg.ffn}x{cfg.hidden} bf16",
+                         "peak_kind": peak_kind},
+            "step_roofline": {"tokens_per_s": roof_tps, "frac": value / roof_tps, "F_tok": F_tok,
+                              "peak_tflops": peak_sust, "peak_kind": f"{peak_kind} sustained",
+                              "beta_ideal": beta_ideal, "model_tflops": value * F_tok / 1e12},
+            "bubble": {"analytic": float(ps.analytic_bubble_ratio(approach, D, N)),
+                       "canonical_of_order": beta_order,
+                       "measured": None if G == 1 else "see rank timelines",
+                       "note": "1 GPU: logical devices share the GPU, so the pipeline bubble is not idle time"},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        if rank == 0 and os.environ.get("BP_SKIP_CPU_BASELINE") != "1":
+            line["cpu_baseline"] = _cpu_baseline(cfg, args)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _cpu_baseline(cfg, args):
+    import torch
+    from oracle.gpt_oracle import OracleConfig, layer_sample_seconds
+    from paper_2410_19367_b200.model import flops_per_token
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    oc = OracleConfig(cfg.layers, cfg.hidden, cfg.heads, cfg.seq, cfg.vocab, cfg.micro_batch, cfg.causal)
+    M = cfg.micro_batch * cfg.seq
+    layer_flops = 3.0 * (24 * cfg.hidden ** 2 + 4 * cfg.seq * cfg.hidden) * M
+    scale = flops_per_token(cfg) * M / layer_flops
+    layer_sample_seconds(oc)
+    t = statistics.median(layer_sample_seconds(oc) for _ in range(3))
+    return {"value": M / (t * scale), "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"fwd+bwd of 1 transformer layer, 1 micro-batch ({M} tokens), fp32 torch CPU (oracle "
+                      f"restatement of SPEC run_schedule_numeric), extrapolated x{scale:.1f} by model FLOPs"}
+
+
+if __name__ == "__main__":
+    main()

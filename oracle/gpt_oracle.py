@@ -253,3 +253,26 @@ def run_schedule_numeric(cfg: OracleConfig, schedule_json: str | dict, params: d
     m0, v0 = adam_state if adam_state is not None else (_zeros_like(base), _zeros_like(base))
     newp, m1, v1 = adamw_update(base, g, m0, v0, cfg, step)
     return StepResult(losses, g, newp, m1, v1)
+
+
+def layer_sample_seconds(cfg: OracleConfig, *, dtype=torch.float32, seed: int = 0) -> float:
+    """CPU wall time of forward + backward of ONE transformer layer (attention
+    half + MLP half) on ONE micro-batch -- the bounded sample the benchmark's
+    CPU baseline extrapolates from (uses torch's intra-op threads)."""
+    import time as _time
+    g = torch.Generator().manual_seed(seed)
+    h, f = cfg.hidden, 4 * cfg.hidden
+    P = {
+        "layers.0.ln1.w": torch.ones(h), "layers.0.ln1.b": torch.zeros(h),
+        "layers.0.attn.qkv.w": torch.randn(3 * h, h, generator=g) * 0.02, "layers.0.attn.qkv.b": torch.zeros(3 * h),
+        "layers.0.attn.proj.w": torch.randn(h, h, generator=g) * 0.02, "layers.0.attn.proj.b": torch.zeros(h),
+        "layers.0.ln2.w": torch.ones(h), "layers.0.ln2.b": torch.zeros(h),
+        "layers.0.mlp.fc1.w": torch.randn(f, h, generator=g) * 0.02, "layers.0.mlp.fc1.b": torch.zeros(f),
+        "layers.0.mlp.fc2.w": torch.randn(h, f, generator=g) * 0.02, "layers.0.mlp.fc2.b": torch.zeros(h),
+    }
+    P = {k: v.to(dtype).requires_grad_(True) for k, v in P.items()}
+    x = torch.randn(cfg.micro_batch, cfg.seq, h, generator=g).to(dtype).requires_grad_(True)
+    t0 = _time.perf_counter()
+    y = _mlp_half(P, 0, _attn_half(P, 0, x, cfg), cfg)
+    y.backward(torch.ones_like(y))
+    return _time.perf_counter() - t0

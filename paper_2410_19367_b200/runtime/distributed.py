@@ -1,0 +1,174 @@
+"""Multi-GPU plumbing of the train step: one process per GPU, rank == logical
+device of the schedule, torch.distributed (NCCL) as the transport.
+
+P2P (activations forward, gradients backward)
+  The reference per-device orders are not FIFO-consistent per link (SURVEY
+  §0 F5), so messages are tag-addressed: every directed link (src -> dst)
+  gets its OWN process group (so the two directions of a device pair never
+  serialise on one NCCL stream), the sender issues ``isend`` in its task
+  order, and the receiver posts ALL of the iteration's ``irecv``s for that
+  link up-front, in the SENDER's order, into slot buffers keyed by
+  (kind, direction, micro-batch, destination stage).  A consumer task only
+  waits (stream-wise) for its own slot.
+
+Eager gradient synchronisation
+  Model stage s lives on dev_down(s) (down replica) and dev_up(s) = D-1-
+  dev_down(s) (up replica).  Each (stage) has its own 2-rank group, so the
+  two ranks may reach their last backward of s in different orders without
+  any collective-ordering constraint.  Right after a rank issues its last
+  backward of s, it issues all_reduce(SUM) of that stage's flat fp32
+  gradient on the optimizer stream followed by the fused AdamW with
+  grad_scale 1/2 (replica mean).  A 2-term fp32 sum is commutative, so both
+  replicas compute bit-identical updates.
+
+All of this is host-side control flow; it runs unchanged on CPU tensors with
+the gloo backend (``cuda=False``), which is how tests/ exercise it.
+"""
+from __future__ import annotations
+
+from contextlib import nullcontext
+
+import torch
+import torch.distributed as dist
+
+from ..schedule import Schedule, TaskKind
+
+__all__ = ["DistContext", "link_messages"]
+
+
+def link_messages(sched: Schedule) -> dict:
+    """{(src, dst): [key, ...]} -- the cross-device messages of one iteration
+    in each sender's production order; key = (kind, direction, mb, dst stage)."""
+    last = sched.num_stages - 1
+    out: dict = {}
+    for src, row in enumerate(sched.per_device):
+        for t in row:
+            smap = sched.stage_map(t.direction)
+            if t.kind is TaskKind.FORWARD and t.stage < last:
+                dst = smap.device_of(t.stage + 1)
+                key = ("act", t.direction, t.micro_batch, t.stage + 1)
+            elif t.kind is TaskKind.BACKWARD and t.stage > 0:
+                dst = smap.device_of(t.stage - 1)
+                key = ("grad", t.direction, t.micro_batch, t.stage - 1)
+            else:
+                continue
+            if dst != src:
+                out.setdefault((src, dst), []).append(key)
+    return out
+
+
+class DistContext:
+    def __init__(self, rank: int, world: int, *, cuda: bool = True):
+        self.rank, self.world, self.cuda = rank, world, cuda
+        self.sched = None
+        self.link_group: dict = {}
+        self.pair_group: dict = {}
+        self.links: dict = {}
+        self.slots: dict = {}
+        self.inflight: list = []
+        self.pending: list = []
+
+    # ----------------------------------------------------------- setup --
+    def build_groups(self, sched: Schedule) -> None:
+        """Create every group in the same order on every rank."""
+        if sched.D != self.world:
+            raise ValueError(f"distributed mode needs world == D (world={self.world}, D={sched.D})")
+        self.sched = sched
+        self.links = link_messages(sched)
+        for (src, dst) in sorted(self.links):
+            self.link_group[(src, dst)] = dist.new_group(sorted({src, dst}))
+        if sched.is_bidirectional:
+            dn, up = sched.stage_maps
+            for s in range(sched.num_stages):
+                a, b = dn.device_of(s), up.device_of(s)
+                self.pair_group[s] = (a, b, dist.new_group(sorted({a, b})))
+
+    # ------------------------------------------------------- primitives --
+    def _sctx(self, stream):
+        return torch.cuda.stream(stream) if (self.cuda and stream is not None) else nullcontext()
+
+    def post_recvs(self, alloc, stream=None) -> None:
+        """Post every receive of this iteration, per incoming link in the
+        sender's order.  ``alloc(key) -> tensor`` provides the slot buffer."""
+        with self._sctx(stream):
+            for (src, dst), keys in sorted(self.links.items()):
+                if dst != self.rank:
+                    continue
+                g = self.link_group[(src, dst)]
+                for key in keys:
+                    buf = alloc(key)
+                    self.slots[key] = (buf, dist.irecv(buf, src, group=g))
+
+    def send(self, key, tensor, dst, stream=None) -> None:
+        with self._sctx(stream):
+            work = dist.isend(tensor, dst, group=self.link_group[(self.rank, dst)])
+        self.inflight.append((tensor, work))
+
+    def recv(self, key, stream=None):
+        item = self.slots.pop(key, None)
+        if item is None:
+            raise RuntimeError(f"protocol violation: rank {self.rank} has no posted receive for {key}")
+        buf, work = item
+        with self._sctx(stream):
+            work.wait()
+        return buf
+
+    def allreduce_stage(self, stage: int, tensor, stream=None) -> bool:
+        """SUM-all-reduce ``tensor`` with the other replica of ``stage``;
+        False if the schedule has no replica pair (unidirectional)."""
+        if stage not in self.pair_group:
+            return False
+        with self._sctx(stream):
+            if self.cuda:   # NCCL: stream-ordered, the host never blocks
+                dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=self.pair_group[stage][2])
+            else:           # gloo: host-blocking collectives would serialise ranks; run async
+                self.pending.append(dist.all_reduce(tensor, op=dist.ReduceOp.SUM,
+                                                    group=self.pair_group[stage][2], async_op=True))
+        return True
+
+    def finish_allreduces(self) -> None:
+        for w in self.pending:
+            w.wait()
+        self.pending.clear()
+
+    def drain_sends(self, stream=None) -> list:
+        """Wait (stream-wise) for all sends; returns the sent buffers."""
+        out = []
+        with self._sctx(stream):
+            for t, w in self.inflight:
+                w.wait()
+                out.append(t)
+        self.inflight.clear()
+        return out
+
+    # --------------------------------------------- Trainer integration --
+    def setup(self, trainer) -> None:
+        self.build_groups(trainer.sched)
+
+    def begin_iteration(self, trainer) -> None:
+        cfg = trainer.cfg
+        shape = (cfg.micro_batch * cfg.seq, cfg.hidden)
+        st = trainer.streams[self.rank]
+        self.post_recvs(lambda key: trainer.pool.get(shape, trainer.dtype, st), stream=st)
+
+    def send_msg(self, trainer, key, tensor, src, dst) -> None:
+        self.send(key, tensor, dst, stream=trainer.streams[src])
+
+    def recv_msg(self, trainer, key, d):
+        return self.recv(key, stream=trainer.streams[d])
+
+    def sync_stage(self, trainer, dr, s, ev) -> None:
+        st = trainer.opt_stream
+        st.wait_event(ev)
+        sp = trainer.stage_params[(dr, s)]
+        paired = self.allreduce_stage(s, sp.grad, stream=st)
+        trainer._adam((dr, s), [sp.grad], [sp.flat], st, grad_scale=0.5 if paired else 1.0)
+
+    def end_iteration(self, trainer) -> None:
+        if self.slots:
+            raise RuntimeError(f"protocol violation: {len(self.slots)} posted receives never consumed")
+        main = torch.cuda.current_stream(trainer.device)
+        sent = self.drain_sends(stream=main)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        trainer.pool.put_all(sent, ev)

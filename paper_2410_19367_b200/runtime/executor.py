@@ -40,7 +40,7 @@ from . import ops
 from .compute import StageCompute
 from .state import BufferPool, StageParams
 
-__all__ = ["Trainer", "StepOutput", "issue_order"]
+__all__ = ["Trainer", "StepOutput", "issue_order", "drive"]
 
 
 @dataclass
@@ -62,6 +62,39 @@ def issue_order(schedule: Schedule):
             items.append((starts[t], d, i, t))
     items.sort(key=lambda x: (x[0], x[1], x[2]))
     return [(d, i, t) for _, d, i, t in items]
+
+
+def drive(order, num_stages, last_b, *, forward, backward, send, recv, stage_done, dev_of):
+    """Issue every task of ``order`` (list of (device, position, Task)).
+
+    Pure host-side control flow shared by the CUDA executor and the
+    multi-process CPU tests: forward(d, t, x0) -> (stash, out|None);
+    backward(d, t, stash, dy) -> (dx|None, event); send/recv move
+    tag-addressed messages keyed (kind, direction, mb, destination stage);
+    stage_done(direction, stage, d, event) fires after the LAST backward of
+    that (direction, stage) on device d -- the eager sync launch point.
+    Returns the leftover (msgs, stashes), both empty for a valid schedule.
+    """
+    msgs: dict = {}
+    stashes: dict = {}
+    last = num_stages - 1
+    for d, i, t in order:
+        dr, s, mb = t.direction, t.stage, t.micro_batch
+        if t.kind is TaskKind.FORWARD:
+            x0 = recv(msgs, ("act", dr, mb, s), d) if s > 0 else None
+            stash, out = forward(d, t, x0)
+            stashes[(dr, mb, s)] = stash
+            if out is not None:
+                send(msgs, ("act", dr, mb, s + 1), out, d, dev_of(dr, s + 1))
+        else:
+            dy = recv(msgs, ("grad", dr, mb, s), d) if s < last else None
+            stash = stashes.pop((dr, mb, s))
+            dx, ev = backward(d, t, stash, dy)
+            if dx is not None:
+                send(msgs, ("grad", dr, mb, s - 1), dx, d, dev_of(dr, s - 1), event=ev)
+            if last_b[d].get((dr, s)) == i:
+                stage_done(dr, s, d, ev)
+    return msgs, stashes
 
 
 class Trainer:
@@ -147,18 +180,17 @@ class Trainer:
             with torch.cuda.stream(st):
                 sp.grad.zero_()
 
-    def _adam(self, stage_key, grads, params_out, stream):
+    def _adam(self, stage_key, grads, params_out, stream, grad_scale=1.0):
         owner = self.opt_owner[stage_key]
         o = self.optim
         ops.adam(owner.master, grads[0], grads[1] if len(grads) > 1 else None, owner.m, owner.v,
                  params_out[0], params_out[1] if len(params_out) > 1 else None,
                  lr=o.lr, beta1=o.beta1, beta2=o.beta2, eps=o.eps, weight_decay=o.weight_decay,
-                 step=self.step_count, stream=stream)
+                 step=self.step_count, grad_scale=grad_scale, stream=stream)
 
     # --------------------------------------------------------------- train step --
     def train_step(self, tokens: torch.Tensor, targets: torch.Tensor) -> StepOutput:
         """tokens/targets: int32 device tensors [N, B, S] already on this GPU."""
-        cfg = self.cfg
         self.step_count += 1
         main = torch.cuda.current_stream(self.device)
         start_ev = torch.cuda.Event()
@@ -173,46 +205,41 @@ class Trainer:
         if self.dist is not None:
             self.dist.begin_iteration(self)
 
-        msgs: dict = {}
-        stashes: dict = {}
         done_dirs: dict = {}
         tl = [] if self.record_timeline else None
-        M = cfg.micro_batch * cfg.seq
-        for d, i, t in self.order:
+
+        def forward(d, t, x0):
             stream = self.streams[d]
-            dr, s, mb = t.direction, t.stage, t.micro_batch
-            comp = self.compute[(dr, s)]
+            comp = self.compute[(t.direction, t.stage)]
+            mb = t.micro_batch
             if tl is not None:
-                ev0 = torch.cuda.Event(enable_timing=True)
-                ev0.record(stream)
-            if t.kind is TaskKind.FORWARD:
-                x0 = None
-                if s > 0:
-                    x0 = self._recv(msgs, ("act", dr, mb, s), d)
-                tok = tokens[mb - 1].reshape(-1)
-                tgt = targets[mb - 1].reshape(-1)
-                stash, out = comp.forward(stream, self.pool, x0=x0, tokens=tok, targets=tgt,
-                                          loss_slot=self.losses[mb - 1:mb])
-                stashes[(dr, mb, s)] = stash
-                if out is not None:
-                    self._send(msgs, ("act", dr, mb, s + 1), out, d, self._dev_of(dr, s + 1))
-            else:
-                dy = None
-                if s < self.S - 1:
-                    dy = self._recv(msgs, ("grad", dr, mb, s), d)
-                stash = stashes.pop((dr, mb, s))
-                dx, release = comp.backward(stream, self.pool, stash, dy, self.ws[d])
-                ev = torch.cuda.Event()
-                ev.record(stream)
-                self.pool.put_all(release, ev)
-                if dx is not None:
-                    self._send(msgs, ("grad", dr, mb, s - 1), dx, d, self._dev_of(dr, s - 1), event=ev)
-                if self.last_b[d].get((dr, s)) == i:
-                    self._stage_grads_ready(dr, s, d, ev, done_dirs)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            res = comp.forward(stream, self.pool, x0=x0, tokens=tokens[mb - 1].reshape(-1),
+                               targets=targets[mb - 1].reshape(-1), loss_slot=self.losses[mb - 1:mb])
             if tl is not None:
-                ev1 = torch.cuda.Event(enable_timing=True)
-                ev1.record(stream)
-                tl.append((d, i, t, ev0, ev1))
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(stream)
+                tl.append((d, t, e0, e1))
+            return res
+
+        def backward(d, t, stash, dy):
+            stream = self.streams[d]
+            if tl is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            dx, release = self.compute[(t.direction, t.stage)].backward(stream, self.pool, stash, dy, self.ws[d])
+            ev = torch.cuda.Event(enable_timing=tl is not None)
+            ev.record(stream)
+            self.pool.put_all(release, ev)
+            if tl is not None:
+                tl.append((d, t, e0, ev))
+            return dx, ev
+
+        msgs, stashes = drive(self.order, self.S, self.last_b, forward=forward, backward=backward,
+                              send=self._send, recv=self._recv,
+                              stage_done=lambda dr, s, d, ev: self._stage_grads_ready(dr, s, d, ev, done_dirs),
+                              dev_of=self._dev_of)
         if stashes or (msgs and self.dist is None):
             raise RuntimeError(f"protocol violation: {len(stashes)} stashes / {len(msgs)} messages left at flush")
         if self.dist is not None:
@@ -232,7 +259,7 @@ class Trainer:
     # ---------------------------------------------------------------- messages --
     def _send(self, msgs, key, tensor, src, dst, event=None):
         if self.dist is not None and dst != src:
-            self.dist.send(self, key, tensor, src, dst)
+            self.dist.send_msg(self, key, tensor, src, dst)
             return
         if event is None:
             event = torch.cuda.Event()
@@ -243,7 +270,7 @@ class Trainer:
         item = msgs.pop(key, None)
         if item is None:
             if self.dist is not None:
-                return self.dist.recv(self, key, d)
+                return self.dist.recv_msg(self, key, d)
             raise RuntimeError(f"protocol violation: task on device {d} needs {key} which was never produced")
         tensor, ev = item
         self.streams[d].wait_event(ev)
@@ -297,9 +324,9 @@ class Trainer:
         if not self.timeline:
             return None
         torch.cuda.synchronize(self.device)
-        first = self.timeline[0][3]
+        first = self.timeline[0][2]
         spans: dict = {}
-        for d, i, t, e0, e1 in self.timeline:
+        for d, t, e0, e1 in self.timeline:
             spans.setdefault(d, []).append((first.elapsed_time(e0), first.elapsed_time(e1)))
         busy = {d: sum(b - a for a, b in v) for d, v in spans.items()}
         start = min(a for v in spans.values() for a, _ in v)
