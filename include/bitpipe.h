@@ -59,7 +59,11 @@ BP_API int bp_tc_available(void);
 BP_API unsigned long long bp_launch_count(void);
 /* Process-wide switches (testing aids): route attention to the exact
  * kernel / GEMMs to the SIMT kernel even when the fast path applies. */
-enum bp_option { BP_OPT_ATTN_EXACT = 1, BP_OPT_GEMM_SIMT = 2 };
+enum bp_option {
+  BP_OPT_ATTN_EXACT = 1, /* 1: exact attention kernel for bf16 too            */
+  BP_OPT_GEMM_SIMT = 2,  /* 1: SIMT GEMM for bf16 too                          */
+  BP_OPT_GEMM_MODE = 3   /* tcgen05 tiling: 0 auto, 1 single-SM, 2 CTA pair    */
+};
 BP_API int bp_set_option(int option, int value);
 
 /* ---------------------------------------------------------------- GEMM --

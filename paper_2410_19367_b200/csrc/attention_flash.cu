@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(NT) fwd_kernel(const __nv_bfloat16* __restrict
   const uint32_t sQ = smem_u32(smem);
   const uint32_t sK0 = sQ + 64 * Dh * 2;
   const uint32_t sV0 = sK0 + 2 * 64 * Dh * 2;
-  const int qt = blockIdx.x, bh = blockIdx.y, b = bh / H, h = bh % H;
+  // heaviest (last, for causal) query tiles first; heads vary fastest
+  const int qt = gridDim.y - 1 - blockIdx.y, bh = blockIdx.x, b = bh / H, h = bh % H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ld = 3LL * H * Dh;
   const __nv_bfloat16* qg = qkv + (int64_t)b * S * ld + h * Dh;
@@ -229,7 +230,8 @@ __global__ void __launch_bounds__(NT) bwd_kernel(const __nv_bfloat16* __restrict
   float* s_lse = reinterpret_cast<float*>(smem + 6 * TILE + 64 * 64 * 2);  // [2][64]
   float* s_del = s_lse + 128;                                            // [2][64]
 
-  const int kt = blockIdx.x, bh = blockIdx.y, b = bh / H, h = bh % H;
+  // heaviest (first, for causal) key tiles first; heads vary fastest
+  const int kt = blockIdx.y, bh = blockIdx.x, b = bh / H, h = bh % H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
   const int64_t ld = 3LL * H * Dh, ldo = (int64_t)H * Dh;
@@ -452,7 +454,7 @@ static int launch_fwd(int B, int S, int H, float scale, const void* qkv, void* o
     BP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem<Dh>()));
     set = true;
   }
-  dim3 grid((S + BR - 1) / BR, B * H);
+  dim3 grid(B * H, (S + BR - 1) / BR);
   k<<<grid, NT, fwd_smem<Dh>(), st>>>((const __nv_bfloat16*)qkv, (__nv_bfloat16*)o, lse, S, H,
                                        scale * 1.4426950408889634f);
   count_launch();
@@ -477,7 +479,7 @@ static int launch_bwd(int B, int S, int H, float scale, const void* qkv, const v
     BP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_smem<Dh>()));
     set = true;
   }
-  dim3 grid((S + BC - 1) / BC, B * H);
+  dim3 grid(B * H, (S + BC - 1) / BC);
   k<<<grid, NT, bwd_smem<Dh>(), st>>>((const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dout, lse, delta,
                                        (__nv_bfloat16*)dqkv, dq, S, H, scale, scale * 1.4426950408889634f);
   count_launch();

@@ -7,24 +7,106 @@ namespace bp {
 void count_launch();
 int num_sms();
 
-// ------------------------------------------------------------ colsum ----
-// out[c] += sum_r x[r, c]; thread per 2 columns, row chunks on grid.y.
-template <typename T>
-__global__ void colsum_kernel(int rows, int cols, const T* __restrict__ x, int64_t ld, int rows_per,
-                              float* __restrict__ out) {
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
-  if (c >= cols) return;
+// ------------------------------------------------------- column sums ----
+// Column reductions over token rows, vectorised: a block is 32 x 8 threads;
+// each thread owns 8 consecutive columns (one 16-byte bf16 vector / two
+// fp32 vectors) and walks rows ty, ty+8, ... of the block's row chunk; the
+// 8 row-groups are reduced in shared memory and each column gets one fp32
+// atomicAdd per block.
+//   MODE 0: out0[c] += sum_r x[r,c]
+//   MODE 1: (LayerNorm parameters) out0[c] += sum_r dy*(x-mean_r)*rstd_r,
+//                                  out1[c] += sum_r dy
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) colred_kernel(int rows, int cols, int rows_per, int vec, const T* __restrict__ a,
+                                                     int64_t lda, const T* __restrict__ x, const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd, float* __restrict__ out0,
+                                                     float* __restrict__ out1) {
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c0 = (blockIdx.x * 32 + tx) * 8;
   const int r0 = blockIdx.y * rows_per, r1 = min(rows, r0 + rows_per);
-  float a = 0.f, b = 0.f;
-  const bool two = c + 1 < cols;
-  for (int r = r0; r < r1; ++r) {
-    const T* p = x + (int64_t)r * ld + c;
-    a += to_f<T>(p[0]);
-    if (two) b += to_f<T>(p[1]);
+  float s0[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, s1[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const bool full = vec && c0 + 8 <= cols;
+  if (c0 < cols) {
+    for (int r = r0 + ty; r < r1; r += 8) {
+      float v[8], w[8];
+      const T* pa = a + (int64_t)r * lda + c0;
+      if (full && sizeof(T) == 2) {
+        const uint4 u = *reinterpret_cast<const uint4*>(pa);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(h[j]);
+          v[2 * j] = f.x;
+          v[2 * j + 1] = f.y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = (c0 + j < cols) ? to_f<T>(pa[j]) : 0.f;
+      }
+      if (MODE == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s0[j] += v[j];
+      } else {
+        const T* px = x + (int64_t)r * cols + c0;
+        if (full && sizeof(T) == 2) {
+          const uint4 u = *reinterpret_cast<const uint4*>(px);
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 f = __bfloat1622float2(h[j]);
+            w[2 * j] = f.x;
+            w[2 * j + 1] = f.y;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) w[j] = (c0 + j < cols) ? to_f<T>(px[j]) : 0.f;
+        }
+        const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          s0[j] += v[j] * (w[j] - mu) * rs;
+          s1[j] += v[j];
+        }
+      }
+    }
   }
-  atomicAdd(&out[c], a);
-  if (two) atomicAdd(&out[c + 1], b);
+  __shared__ float red[2][8][32 * 8 + 1];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    red[0][ty][tx * 8 + j] = s0[j];
+    if (MODE == 1) red[1][ty][tx * 8 + j] = s1[j];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256 * (MODE + 1); i += 256) {
+    const int which = i / 256, cc = i % 256;
+    float t = 0.f;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) t += red[which][y][cc];
+    const int col = blockIdx.x * 256 + cc;
+    if (col < cols) atomicAdd(which == 0 ? &out0[col] : &out1[col], t);
+  }
 }
+
+template <typename T, int MODE>
+int launch_colred(int rows, int cols, const void* a, int64_t lda, const void* x, const float* mean, const float* rstd,
+                  float* out0, float* out1, cudaStream_t st) {
+  const int cblocks = (cols + 255) / 256;
+  int chunks = (2 * num_sms() + cblocks - 1) / cblocks;
+  int rows_per = (rows + chunks - 1) / chunks;
+  if (rows_per < 32) rows_per = 32;
+  dim3 grid(cblocks, (rows + rows_per - 1) / rows_per);
+  const int vec = (reinterpret_cast<uintptr_t>(a) % 16 == 0) && (lda % 8 == 0) &&
+                  (!x || (reinterpret_cast<uintptr_t>(x) % 16 == 0 && cols % 8 == 0));
+  colred_kernel<T, MODE><<<grid, 256, 0, st>>>(rows, cols, rows_per, vec, (const T*)a, lda, (const T*)x, mean, rstd,
+                                               out0, out1);
+  count_launch();
+  BP_CHECK_LAUNCH("colred");
+  return BP_OK;
+}
+template int launch_colred<float, 1>(int, int, const void*, int64_t, const void*, const float*, const float*,
+                                     float*, float*, cudaStream_t);
+template int launch_colred<__nv_bfloat16, 1>(int, int, const void*, int64_t, const void*, const float*,
+                                             const float*, float*, float*, cudaStream_t);
 
 // ------------------------------------------------------------- embed ----
 template <typename T>
@@ -186,18 +268,9 @@ extern "C" int bp_colsum_acc(int dtype, int rows, int cols, const void* x, int64
     return BP_ERR_INVALID;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  const int cblocks = (cols + 511) / 512;
-  int chunks = (2 * num_sms() + cblocks - 1) / cblocks;
-  int rows_per = (rows + chunks - 1) / chunks;
-  if (rows_per < 8) rows_per = 8;
-  dim3 grid(cblocks, (rows + rows_per - 1) / rows_per);
-  if (dtype == BP_F32)
-    colsum_kernel<float><<<grid, 256, 0, st>>>(rows, cols, (const float*)x, ldx, rows_per, out);
-  else
-    colsum_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(rows, cols, (const __nv_bfloat16*)x, ldx, rows_per, out);
-  count_launch();
-  BP_CHECK_LAUNCH("colsum");
-  return BP_OK;
+  return dtype == BP_F32
+             ? launch_colred<float, 0>(rows, cols, x, ldx, nullptr, nullptr, nullptr, out, nullptr, st)
+             : launch_colred<__nv_bfloat16, 0>(rows, cols, x, ldx, nullptr, nullptr, nullptr, out, nullptr, st);
 }
 
 extern "C" int bp_embed_fwd(int dtype, int B, int S, int H, const int32_t* tokens, const void* wte, const void* wpe,

@@ -149,6 +149,67 @@ BP_DEV void epi_row32(const Epi& ep, int r, int c0, float (&v)[32]) {
   store32(ep.C, ep.c_dtype, o, v);
 }
 
+// Epilogue of one accumulator tile slice: 32 TMEM lanes (rows) x ncols
+// columns for the calling warp.  The extra global input of the epilogue
+// (fp32 C for accumulation, the residual, or the saved pre-activation for
+// dGELU) of chunk c+1 is loaded while chunk c is finished, so the DRAM
+// latency of the read-modify-write is not serialised across chunks.
+template <int NCHUNK>
+BP_DEV void epi_tile(const Epi& ep, uint32_t tmem_addr, int row, int n0) {
+  const void* xin = nullptr;
+  int xdt = ep.c_dtype;
+  int64_t xld = 0;
+  if (ep.accumulate) {
+    xin = ep.C; xdt = BP_F32; xld = ep.ldc;
+  } else if (ep.residual) {
+    xin = ep.residual; xld = ep.ldr;
+  } else if (ep.epilogue == BP_EPI_DGELU) {
+    xin = ep.aux; xld = ep.ldaux;
+  }
+  // must be warp-uniform: tcgen05.ld below is a .sync.aligned warp collective
+  const bool fast = __all_sync(0xffffffffu, ep.vec_ok && row < ep.M && n0 + NCHUNK * 32 <= ep.N &&
+                                                xin != nullptr &&
+                                                !(ep.residual && (ep.accumulate || ep.epilogue == BP_EPI_DGELU)));
+  if (!fast) {
+#pragma unroll 1
+    for (int c = 0; c < NCHUNK; ++c) {
+      float v[32];
+      tmem_ld_32x32b_x32(tmem_addr + c * 32, v);
+      if (n0 + c * 32 < ep.N) epi_row32(ep, row, n0 + c * 32, v);
+    }
+    return;
+  }
+  const int64_t xrow = (int64_t)row * xld + n0;
+  float nxt[32];
+  load32(xin, xdt, xrow, nxt);
+#pragma unroll 1
+  for (int c = 0; c < NCHUNK; ++c) {
+    float cur[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) cur[i] = nxt[i];
+    if (c + 1 < NCHUNK) load32(xin, xdt, xrow + (c + 1) * 32, nxt);
+    float v[32];
+    tmem_ld_32x32b_x32(tmem_addr + c * 32, v);
+    const int c0 = n0 + c * 32;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= ep.alpha;
+    if (ep.bias) {
+      float t[32];
+      load32(ep.bias, ep.bias_dtype, c0, t);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += t[i];
+    }
+    if (ep.epilogue == BP_EPI_DGELU) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(cur[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += cur[i];
+    }
+    store32(ep.C, ep.c_dtype, (int64_t)row * ep.ldc + c0, v);
+  }
+}
+
 // ===================================================== tcgen05 kernel ====
 template <int BN>
 struct TcCfg {
@@ -273,18 +334,162 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       tc_fence_after();
       const int row = m0 + ew * 32 + lane;
       const uint32_t t0 = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        float v[32];
-        tmem_ld_32x32b_x32(t0 + c * 32, v);
-        if (n0 + c * 32 < N) epi_row32(ep, row, n0 + c * 32, v);
-      }
+      epi_tile<BN / 32>(ep, t0, row, n0);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
   }
   __syncthreads();
   if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
+}
+
+
+// ============================================ tcgen05 2-SM (CTA pair) ====
+// Pair tile 256 x 256: each CTA of the cluster holds 128 rows of A and 128
+// rows (N-half) of B per stage; the leader issues tcgen05.mma.cta_group::2
+// (M=256, N=256) reading both CTAs' smem, each CTA's TMEM receives its own
+// 128 x 256 accumulator.  Halves the per-SM operand traffic of the 1-SM
+// kernel (L2 -> SM bandwidth is the bound there).
+struct Tc2Cfg {
+  static constexpr int BM = 128, BN = 256, BNH = 128, BK = 64, STAGES = 6;
+  static constexpr uint32_t A_BYTES = BM * BK * 2;
+  static constexpr uint32_t B_BYTES = BNH * BK * 2;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static constexpr size_t SMEM = 1024 + STAGES * (size_t)STAGE_BYTES + 256;
+};
+
+template <bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                int M, int N, int K, Epi ep) {
+  using C = Tc2Cfg;
+  constexpr int BK = C::BK, STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int tiles_m = (M + 255) / 256, tiles_n = (N + C::BN - 1) / C::BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int kblocks = (K + BK - 1) / BK;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 2);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 256);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_2sm<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // -------------------------- TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
+        const int m0 = (tile % tiles_m) * 256 + rank * 128;
+        const int n0 = (tile / tiles_m) * C::BN + rank * C::BNH;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* a = sA + stage * C::A_BYTES;
+          uint8_t* b = sB + stage * C::B_BYTES;
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_2d_2sm(a, &map_a, k0, m0, &full[stage]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) tma_load_2d_2sm(a + c * (BK * 128), &map_a, m0 + 64 * c, k0, &full[stage]);
+          }
+          if (!B_MN) {
+            tma_load_2d_2sm(b, &map_b, k0, n0, &full[stage]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) tma_load_2d_2sm(b + c * (BK * 128), &map_b, n0 + 64 * c, k0, &full[stage]);
+          }
+          if (leader)
+            mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+          else
+            mbar_arrive_remote(&full[stage], 0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only)
+      constexpr uint32_t idesc = umma_idesc_bf16(256, C::BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * C::BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? umma_desc_sw128(a_addr + k * 2048, BK * 128, 1024)
+                                     : umma_desc_sw128(a_addr + k * 32, 0, 1024);
+            const uint64_t bd = B_MN ? umma_desc_sw128(b_addr + k * 2048, BK * 128, 1024)
+                                     : umma_desc_sw128(b_addr + k * 32, 0, 1024);
+            tc_mma_f16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc_commit_2sm_mc(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit_2sm_mc(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {  // ---------------------- epilogue (both CTAs)
+    const int ew = warp - 4;
+    int it = 0;
+    for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      const int m0 = (tile % tiles_m) * 256 + rank * 128;
+      const int n0 = (tile / tiles_m) * C::BN;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m0 + ew * 32 + lane;
+      const uint32_t t0 = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * C::BN;
+      epi_tile<C::BN / 32>(ep, t0, row, n0);
+      tc_fence_before();
+      if (leader)
+        mbar_arrive(&tempty[acc]);
+      else
+        mbar_arrive_remote(&tempty[acc], 0);
+    }
+  }
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) tmem_dealloc_2sm<C::TMEM_COLS>(tmem_base);
 }
 
 // ======================================================== SIMT kernel ====
@@ -383,6 +588,7 @@ static int make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t 
 void count_launch();
 int num_sms();
 bool opt_gemm_simt();
+int gemm_mode();
 
 template <int BN, bool A_MN, bool B_MN>
 static int launch_tc(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
@@ -420,6 +626,45 @@ static int dispatch_tc(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   if (!amn && bmn) return launch_tc<BN, false, true>(g, ep, st);
   if (amn && !bmn) return launch_tc<BN, true, false>(g, ep, st);
   return launch_tc<BN, true, true>(g, ep, st);
+}
+
+
+template <bool A_MN, bool B_MN>
+static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
+  using C = Tc2Cfg;
+  CUtensorMap ma, mb;
+  int rc;
+  if (!A_MN)
+    rc = make_map(&ma, g.A, g.K, g.M, g.lda, 64, 128);
+  else
+    rc = make_map(&ma, g.A, g.M, g.K, g.lda, 64, 64);
+  if (rc) return rc;
+  if (!B_MN)
+    rc = make_map(&mb, g.B, g.K, g.N, g.ldb, 64, C::BNH);
+  else
+    rc = make_map(&mb, g.B, g.N, g.K, g.ldb, 64, 64);
+  if (rc) return rc;
+  auto kern = gemm_tc2_kernel<A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    BP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr_set = true;
+  }
+  const int tiles = ((g.M + 255) / 256) * ((g.N + C::BN - 1) / C::BN);
+  const int pairs = num_sms() / 2;
+  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  kern<<<grid, 256, C::SMEM, st>>>(ma, mb, g.M, g.N, g.K, ep);
+  count_launch();
+  BP_CHECK_LAUNCH("gemm_tc2");
+  return BP_OK;
+}
+
+static int dispatch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
+  const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
+  if (!amn && !bmn) return launch_tc2<false, false>(g, ep, st);
+  if (!amn && bmn) return launch_tc2<false, true>(g, ep, st);
+  if (amn && !bmn) return launch_tc2<true, false>(g, ep, st);
+  return launch_tc2<true, true>(g, ep, st);
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -461,6 +706,8 @@ extern "C" int bp_gemm(const bp_gemm_args* gp, void* stream) {
       set_error("bp_gemm: bf16 operands need 16-byte aligned bases and ld %% 8 == 0");
       return BP_ERR_INVALID;
     }
+    const int mode = gemm_mode();
+    if (mode == 2 || (mode == 0 && g.M >= 256 && g.N >= 256)) return dispatch_tc2(g, ep, st);
     const int tiles256 = ((g.M + 127) / 128) * ((g.N + 255) / 256);
     if (g.N > 128 && tiles256 >= num_sms()) return dispatch_tc<256>(g, ep, st);
     return dispatch_tc<128>(g, ep, st);

@@ -11,6 +11,9 @@
 namespace bp {
 void count_launch();
 int num_sms();
+template <typename T, int MODE>
+int launch_colred(int rows, int cols, const void* a, int64_t lda, const void* x, const float* mean, const float* rstd,
+                  float* out0, float* out1, cudaStream_t st);
 
 template <typename T>
 struct Vec;  // 16-byte vector of T
@@ -298,18 +301,8 @@ static int ln_bwd_t(int rows, int cols, const void* dy, const void* x, const voi
       ln_bwd_generic_dx<T><<<rows, 256, 0, st>>>(cols, DY, X, G, mean, rstd, R, DX);
   }
   count_launch();
-  {
-    // column sums for dgamma / dbeta: enough row chunks to fill the GPU
-    int chunks = (2 * num_sms() * 256 + cols - 1) / cols;
-    if (chunks < 1) chunks = 1;
-    int rows_per = (rows + chunks - 1) / chunks;
-    if (rows_per < 16) rows_per = 16;
-    dim3 grid((cols + 255) / 256, (rows + rows_per - 1) / rows_per);
-    ln_bwd_generic_params<T><<<grid, 256, 0, st>>>(rows, cols, rows_per, DY, X, mean, rstd, dgamma, dbeta);
-    count_launch();
-  }
-  BP_CHECK_LAUNCH("ln_bwd");
-  return BP_OK;
+  BP_CHECK_LAUNCH("ln_bwd_dx");
+  return launch_colred<T, 1>(rows, cols, dy, cols, x, mean, rstd, dgamma, dbeta, st);
 }
 
 }  // namespace bp

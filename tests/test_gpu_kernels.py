@@ -30,9 +30,17 @@ SHAPES = [(128, 128, 64), (256, 512, 128), (300, 200, 192), (2048, 6144, 2048), 
           (512, 50304 // 8, 256), (130, 136, 72)]
 
 
+@pytest.fixture(params=[1, 2], ids=["1sm", "2sm"])
+def gemm_mode(request):
+    from paper_2410_19367_b200.runtime.lib import OPT_GEMM_MODE
+    ops.set_option(OPT_GEMM_MODE, request.param)
+    yield request.param
+    ops.set_option(OPT_GEMM_MODE, 0)
+
+
 @pytest.mark.parametrize("M,N,K", SHAPES)
 @pytest.mark.parametrize("ak,bk", [(True, True), (True, False), (False, False), (False, True)])
-def test_gemm_bf16_tc(M, N, K, ak, bk):
+def test_gemm_bf16_tc(M, N, K, ak, bk, gemm_mode):
     if (not ak and M % 8) or (not bk and N % 8) or K % 8:
         pytest.skip("TMA needs 16-byte row pitches")
     dev = "cuda"
@@ -53,8 +61,8 @@ def test_gemm_bf16_tc(M, N, K, ak, bk):
     assert _relerr(C32, base + 0.5 * ref) < 2e-5 * math.sqrt(K) + 1e-4
 
 
-@pytest.mark.parametrize("M,N,K", [(256, 512, 128), (300, 264, 96)])
-def test_gemm_epilogues(M, N, K):
+@pytest.mark.parametrize("M,N,K", [(256, 512, 128), (300, 264, 96), (512, 768, 256)])
+def test_gemm_epilogues(M, N, K, gemm_mode):
     dev = "cuda"
     X = torch.randn(M, K, device=dev).bfloat16()
     W = torch.randn(N, K, device=dev).bfloat16()
