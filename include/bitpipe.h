@@ -60,7 +60,8 @@ BP_API unsigned long long bp_launch_count(void);
 /* Process-wide switches (testing aids): route attention to the exact
  * kernel / GEMMs to the SIMT kernel even when the fast path applies. */
 enum bp_option {
-  BP_OPT_ATTN_EXACT = 1, /* 1: exact attention kernel for bf16 too            */
+  BP_OPT_ATTN_EXACT = 1, /* attention impl: 0 auto (tcgen05 > mma.sync flash
+                            > exact), 1 exact kernel, 2 mma.sync flash       */
   BP_OPT_GEMM_SIMT = 2,  /* 1: SIMT GEMM for bf16 too                          */
   BP_OPT_GEMM_MODE = 3   /* tcgen05 tiling: 0 auto, 1 single-SM, 2 CTA pair    */
 };

@@ -18,6 +18,11 @@ int attn_flash_fwd(int B, int S, int H, int Dh, int causal, float scale, const v
 int attn_flash_bwd(int B, int S, int H, int Dh, int causal, float scale, const void* qkv, const void* o,
                    const void* dout, const float* lse, void* dqkv, float* ws, cudaStream_t st);
 bool attn_flash_supported(int dtype, int S, int Dh);
+bool attn_tc_supported(int dtype, int S, int Dh);
+int attn_tc_fwd(int B, int S, int H, int Dh, int causal, float scale, const void* qkv, void* o, float* lse,
+                cudaStream_t st);
+int attn_tc_bwd(int B, int S, int H, int Dh, int causal, float scale, const void* qkv, const void* o,
+                const void* dout, const float* lse, void* dqkv, float* ws, cudaStream_t st);
 
 constexpr int kMaxDhPerLane = 4;  // Dh <= 128
 
@@ -205,6 +210,7 @@ extern "C" int bp_attn_fwd(int dtype, int B, int S, int H, int Dh, int causal, f
                            float* lse, void* stream) {
   if (int rc = attn_check(B, S, H, Dh)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  if (attn_tc_supported(dtype, S, Dh)) return attn_tc_fwd(B, S, H, Dh, causal, scale, qkv, o, lse, st);
   if (attn_flash_supported(dtype, S, Dh)) return attn_flash_fwd(B, S, H, Dh, causal, scale, qkv, o, lse, st);
   return dtype == BP_F32 ? fwd_exact<float>(B, S, H, Dh, causal, scale, qkv, o, lse, st)
                          : fwd_exact<__nv_bfloat16>(B, S, H, Dh, causal, scale, qkv, o, lse, st);
@@ -215,6 +221,8 @@ extern "C" int bp_attn_bwd(int dtype, int B, int S, int H, int Dh, int causal, f
                            void* stream) {
   if (int rc = attn_check(B, S, H, Dh)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  if (attn_tc_supported(dtype, S, Dh))
+    return attn_tc_bwd(B, S, H, Dh, causal, scale, qkv, o, dout, lse, dqkv, workspace, st);
   if (attn_flash_supported(dtype, S, Dh))
     return attn_flash_bwd(B, S, H, Dh, causal, scale, qkv, o, dout, lse, dqkv, workspace, st);
   return dtype == BP_F32 ? bwd_exact<float>(B, S, H, Dh, causal, scale, qkv, o, dout, lse, dqkv, workspace, st)

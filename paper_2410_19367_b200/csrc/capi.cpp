@@ -40,7 +40,8 @@ int num_sms() {
   return cached;
 }
 
-bool opt_attn_exact() { return g_opt_attn_exact.load() != 0; }
+bool opt_attn_exact() { return g_opt_attn_exact.load() == 1; }
+bool opt_attn_no_tc() { return g_opt_attn_exact.load() != 0; }
 bool opt_gemm_simt() { return g_opt_gemm_simt.load() != 0; }
 int gemm_mode() { return g_opt_gemm_mode.load(); }
 

@@ -138,35 +138,47 @@ __global__ void embed_bwd_pos_kernel(int B, int S, int H, const T* __restrict__ 
 }
 
 // --------------------------------------------------------------- xent ----
-// Block per row.  Pass 1: online max / sum-exp.  Pass 2: write the scaled
-// gradient in place.  Loss uses logsumexp - logit[target].
+// Block per row.  Pass 1: online max / sum-exp over 16-byte vectors.
+// Pass 2: re-read (L2-resident), write the scaled gradient in place.
+// Loss uses logsumexp - logit[target].
+BP_DEV void lse_combine(float& m, float& s, float m2, float s2) {
+  const float mm = fmaxf(m, m2);
+  s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+  m = mm;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(512) xent_kernel(int V, T* __restrict__ logits, int64_t ld,
                                                    const int32_t* __restrict__ tgt, float grad_scale,
-                                                   float loss_scale, float* __restrict__ loss) {
+                                                   float loss_scale, float* __restrict__ loss, int vec) {
   const int r = blockIdx.x;
   T* row = logits + (int64_t)r * ld;
+  constexpr int E = 16 / sizeof(T);
+  const int nv = vec ? V / E : 0;
   float m = -INFINITY, s = 0.f;
-  for (int c = threadIdx.x; c < V; c += blockDim.x) {
-    const float x = to_f<T>(row[c]);
-    if (x > m) {
-      s = s * __expf(m - x) + 1.f;
-      m = x;
-    } else {
-      s += __expf(x - m);
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    const uint4 u = reinterpret_cast<const uint4*>(row)[i];
+    const T* e = reinterpret_cast<const T*>(&u);
+    float x[E], mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      x[j] = to_f<T>(e[j]);
+      mx = fmaxf(mx, x[j]);
     }
+    float t = 0.f;
+#pragma unroll
+    for (int j = 0; j < E; ++j) t += __expf(x[j] - mx);
+    lse_combine(m, s, mx, t);
   }
-  // combine (m, s) across the warp then the block
+  for (int c = nv * E + threadIdx.x; c < V; c += blockDim.x) lse_combine(m, s, to_f<T>(row[c]), 1.f);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
     const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
-    const float mm = fmaxf(m, m2);
-    s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
-    m = mm;
+    lse_combine(m, s, m2, s2);
   }
   __shared__ float sm[32], ss[32];
-  __shared__ float g_m, g_lse;
+  __shared__ float g_lse;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) {
     sm[w] = m;
@@ -174,20 +186,26 @@ __global__ void __launch_bounds__(512) xent_kernel(int V, T* __restrict__ logits
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    float M = -INFINITY;
+    float M = -INFINITY, S = 0.f;
     const int nw = blockDim.x >> 5;
-    for (int i = 0; i < nw; ++i) M = fmaxf(M, sm[i]);
-    float S = 0.f;
-    for (int i = 0; i < nw; ++i) S += ss[i] == 0.f ? 0.f : ss[i] * __expf(sm[i] - M);
-    g_m = M;
+    for (int i = 0; i < nw; ++i) lse_combine(M, S, sm[i], ss[i]);
     g_lse = M + logf(S);
-    const int t = tgt[r];
-    atomicAdd(loss, loss_scale * (g_lse - to_f<T>(row[t])));
+    atomicAdd(loss, loss_scale * (g_lse - to_f<T>(row[tgt[r]])));
   }
   __syncthreads();
   const float lse = g_lse;
   const int t = tgt[r];
-  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    uint4 u = reinterpret_cast<const uint4*>(row)[i];
+    T* e = reinterpret_cast<T*>(&u);
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int c = i * E + j;
+      e[j] = from_f<T>((__expf(to_f<T>(e[j]) - lse) - (c == t ? 1.f : 0.f)) * grad_scale);
+    }
+    reinterpret_cast<uint4*>(row)[i] = u;
+  }
+  for (int c = nv * E + threadIdx.x; c < V; c += blockDim.x) {
     const float p = __expf(to_f<T>(row[c]) - lse);
     row[c] = from_f<T>((p - (c == t ? 1.f : 0.f)) * grad_scale);
   }
@@ -309,11 +327,14 @@ extern "C" int bp_xent_fwd_bwd(int dtype, int rows, int V, void* logits, int64_t
                                float grad_scale, float loss_scale, float* loss_out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int threads = V >= 4096 ? 512 : 128;
+  const int esz = dtype == BP_F32 ? 4 : 2;
+  const int vec = (reinterpret_cast<uintptr_t>(logits) % 16 == 0) && ((ld * esz) % 16 == 0);
   if (dtype == BP_F32)
-    xent_kernel<float><<<rows, threads, 0, st>>>(V, (float*)logits, ld, targets, grad_scale, loss_scale, loss_out);
+    xent_kernel<float><<<rows, threads, 0, st>>>(V, (float*)logits, ld, targets, grad_scale, loss_scale, loss_out,
+                                                 vec);
   else
     xent_kernel<__nv_bfloat16><<<rows, threads, 0, st>>>(V, (__nv_bfloat16*)logits, ld, targets, grad_scale,
-                                                          loss_scale, loss_out);
+                                                          loss_scale, loss_out, vec);
   count_launch();
   BP_CHECK_LAUNCH("xent");
   return BP_OK;

@@ -563,8 +563,8 @@ static EncodeTiledFn encode_fn() {
 
 // bf16 2-D map over a row-major matrix with `inner` contiguous elements per
 // row (row pitch `ld` elements) and `outer` rows; box = box_inner x box_outer.
-static int make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, int64_t ld,
-                    uint32_t box_inner, uint32_t box_outer) {
+int make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, int64_t ld,
+             uint32_t box_inner, uint32_t box_outer) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");

@@ -235,15 +235,17 @@ def test_adam_matches_torch():
     assert torch.equal(pa, pb) and torch.equal(pa, master.bfloat16())
 
 
-@pytest.mark.parametrize("S,Dh,causal", [(512, 128, True), (256, 64, False)])
+@pytest.mark.parametrize("S,Dh,causal", [(512, 128, True), (256, 64, False), (2048, 128, True), (384, 64, True),
+                                         (256, 128, False)])
 def test_flash_matches_exact_path(S, Dh, causal):
-    """bf16 flash kernels vs the exact kernel on identical bf16 inputs."""
+    """bf16 tcgen05 kernels (0) and mma.sync flash kernels (2) vs the exact
+    kernel (1) on identical bf16 inputs."""
     from paper_2410_19367_b200.runtime.lib import OPT_ATTN_EXACT
     B, H = 2, 2
     scale = 1.0 / math.sqrt(Dh)
     qkv = torch.randn(B * S, 3 * H * Dh, device="cuda").bfloat16()
     outs = []
-    for exact in (0, 1):
+    for exact in (0, 2, 1):
         ops.set_option(OPT_ATTN_EXACT, exact)
         try:
             o = torch.empty(B * S, H * Dh, device="cuda", dtype=torch.bfloat16)
@@ -257,5 +259,10 @@ def test_flash_matches_exact_path(S, Dh, causal):
             outs.append((o.float(), lse.clone(), dqkv.float()))
         finally:
             ops.set_option(OPT_ATTN_EXACT, 0)
-    (o1, l1, d1), (o2, l2, d2) = outs
-    assert _relerr(o1, o2) < 1e-2 and _relerr(l1, l2) < 1e-4 and _relerr(d1, d2) < 2e-2
+    (o0, l0, d0), (o1, l1, d1), (o2, l2, d2) = outs
+    for o, l, d in ((o0, l0, d0), (o1, l1, d1)):
+        assert _relerr(o, o2) < 1e-2 and _relerr(l, l2) < 1e-4 and _relerr(d, d2) < 2e-2
+    hd = H * Dh
+    for part in range(3):   # q, k, v gradient blocks separately
+        sl = slice(part * hd, (part + 1) * hd)
+        assert _relerr(d0[:, sl], d2[:, sl]) < 2e-2, part
