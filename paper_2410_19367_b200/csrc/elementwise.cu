@@ -26,46 +26,47 @@ __global__ void __launch_bounds__(256) colred_kernel(int rows, int cols, int row
   const int r0 = blockIdx.y * rows_per, r1 = min(rows, r0 + rows_per);
   float s0[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, s1[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   const bool full = vec && c0 + 8 <= cols;
-  if (c0 < cols) {
-    for (int r = r0 + ty; r < r1; r += 8) {
-      float v[8], w[8];
-      const T* pa = a + (int64_t)r * lda + c0;
-      if (full && sizeof(T) == 2) {
-        const uint4 u = *reinterpret_cast<const uint4*>(pa);
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+  auto load8 = [&](const T* p, float (&v)[8]) {
+    if (full && sizeof(T) == 2) {
+      const uint4 u = *reinterpret_cast<const uint4*>(p);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f = __bfloat1622float2(h[j]);
-          v[2 * j] = f.x;
-          v[2 * j + 1] = f.y;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = (c0 + j < cols) ? to_f<T>(pa[j]) : 0.f;
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        v[2 * j] = f.x;
+        v[2 * j + 1] = f.y;
       }
-      if (MODE == 0) {
+    } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) s0[j] += v[j];
-      } else {
-        const T* px = x + (int64_t)r * cols + c0;
-        if (full && sizeof(T) == 2) {
-          const uint4 u = *reinterpret_cast<const uint4*>(px);
-          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+      for (int j = 0; j < 8; ++j) v[j] = (c0 + j < cols) ? to_f<T>(p[j]) : 0.f;
+    }
+  };
+  if (c0 < cols) {
+    // 4 independent rows (8 apart) per iteration keep 4 loads in flight
+    for (int rb = r0 + ty; rb < r1; rb += 32) {
+      float v[4][8], w[4][8];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float2 f = __bfloat1622float2(h[j]);
-            w[2 * j] = f.x;
-            w[2 * j + 1] = f.y;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) w[j] = (c0 + j < cols) ? to_f<T>(px[j]) : 0.f;
+      for (int k = 0; k < 4; ++k) {
+        const int r = rb + 8 * k;
+        if (r < r1) {
+          load8(a + (int64_t)r * lda + c0, v[k]);
+          if (MODE == 1) load8(x + (int64_t)r * cols + c0, w[k]);
         }
-        const float mu = mean[r], rs = rstd[r];
+      }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          s0[j] += v[j] * (w[j] - mu) * rs;
-          s1[j] += v[j];
+      for (int k = 0; k < 4; ++k) {
+        const int r = rb + 8 * k;
+        if (r >= r1) continue;
+        if (MODE == 0) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) s0[j] += v[k][j];
+        } else {
+          const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            s0[j] += v[k][j] * (w[k][j] - mu) * rs;
+            s1[j] += v[k][j];
+          }
         }
       }
     }

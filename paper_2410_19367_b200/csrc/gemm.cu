@@ -350,8 +350,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 // (M=256, N=256) reading both CTAs' smem, each CTA's TMEM receives its own
 // 128 x 256 accumulator.  Halves the per-SM operand traffic of the 1-SM
 // kernel (L2 -> SM bandwidth is the bound there).
+template <int BN_>
 struct Tc2Cfg {
-  static constexpr int BM = 128, BN = 256, BNH = 128, BK = 64, STAGES = 6;
+  static constexpr int BM = 128, BN = BN_, BNH = BN_ / 2, BK = 64, STAGES = BN_ == 256 ? 6 : 8;
   static constexpr uint32_t A_BYTES = BM * BK * 2;
   static constexpr uint32_t B_BYTES = BNH * BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -359,11 +360,11 @@ struct Tc2Cfg {
   static constexpr size_t SMEM = 1024 + STAGES * (size_t)STAGE_BYTES + 256;
 };
 
-template <bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 int M, int N, int K, Epi ep) {
-  using C = Tc2Cfg;
+  using C = Tc2Cfg<BN>;
   constexpr int BK = C::BK, STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -426,7 +427,8 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             tma_load_2d_2sm(b, &map_b, k0, n0, &full[stage]);
           } else {
 #pragma unroll
-            for (int c = 0; c < 2; ++c) tma_load_2d_2sm(b + c * (BK * 128), &map_b, n0 + 64 * c, k0, &full[stage]);
+            for (int c = 0; c < C::BNH / 64; ++c)
+              tma_load_2d_2sm(b + c * (BK * 128), &map_b, n0 + 64 * c, k0, &full[stage]);
           }
           if (leader)
             mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
@@ -629,9 +631,9 @@ static int dispatch_tc(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
 }
 
 
-template <bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN>
 static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
-  using C = Tc2Cfg;
+  using C = Tc2Cfg<BN>;
   CUtensorMap ma, mb;
   int rc;
   if (!A_MN)
@@ -644,7 +646,7 @@ static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   else
     rc = make_map(&mb, g.B, g.N, g.K, g.ldb, 64, 64);
   if (rc) return rc;
-  auto kern = gemm_tc2_kernel<A_MN, B_MN>;
+  auto kern = gemm_tc2_kernel<BN, A_MN, B_MN>;
   static bool attr_set = false;
   if (!attr_set) {
     BP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -659,12 +661,23 @@ static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   return BP_OK;
 }
 
-static int dispatch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
+template <int BN>
+static int dispatch_tc2_bn(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
-  if (!amn && !bmn) return launch_tc2<false, false>(g, ep, st);
-  if (!amn && bmn) return launch_tc2<false, true>(g, ep, st);
-  if (amn && !bmn) return launch_tc2<true, false>(g, ep, st);
-  return launch_tc2<true, true>(g, ep, st);
+  if (!amn && !bmn) return launch_tc2<BN, false, false>(g, ep, st);
+  if (!amn && bmn) return launch_tc2<BN, false, true>(g, ep, st);
+  if (amn && !bmn) return launch_tc2<BN, true, false>(g, ep, st);
+  return launch_tc2<BN, true, true>(g, ep, st);
+}
+
+// Pair tile 256 x 256 unless that leaves the GPU under one wave of pairs,
+// then 256 x 128 (twice the tiles, so each pair overlaps one tile's
+// epilogue with the next tile's MMAs).
+static int dispatch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
+  const int pairs = num_sms() / 2;
+  const int t256 = ((g.M + 255) / 256) * ((g.N + 255) / 256);
+  if (t256 < pairs && g.N >= 128) return dispatch_tc2_bn<128>(g, ep, st);
+  return dispatch_tc2_bn<256>(g, ep, st);
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
