@@ -63,7 +63,9 @@ enum bp_option {
   BP_OPT_ATTN_EXACT = 1, /* attention impl: 0 auto (tcgen05 > mma.sync flash
                             > exact), 1 exact kernel, 2 mma.sync flash       */
   BP_OPT_GEMM_SIMT = 2,  /* 1: SIMT GEMM for bf16 too                          */
-  BP_OPT_GEMM_MODE = 3   /* tcgen05 tiling: 0 auto, 1 single-SM, 2 CTA pair    */
+  BP_OPT_GEMM_MODE = 3,  /* tcgen05 tiling: 0 auto, 1 single-SM, 2 CTA pair    */
+  BP_OPT_STREAM_K = 4    /* 1: stream-K split of the last GEMM wave (default 0:
+                            measured slower on the GPT-1.3B shapes)          */
 };
 BP_API int bp_set_option(int option, int value);
 

@@ -12,7 +12,7 @@ namespace bp {
 
 static thread_local char g_err[1024] = "";
 static std::atomic<unsigned long long> g_launches{0};
-static std::atomic<int> g_opt_attn_exact{0}, g_opt_gemm_simt{0}, g_opt_gemm_mode{0};
+static std::atomic<int> g_opt_attn_exact{0}, g_opt_gemm_simt{0}, g_opt_gemm_mode{0}, g_opt_stream_k{0};
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -44,6 +44,7 @@ bool opt_attn_exact() { return g_opt_attn_exact.load() == 1; }
 bool opt_attn_no_tc() { return g_opt_attn_exact.load() != 0; }
 bool opt_gemm_simt() { return g_opt_gemm_simt.load() != 0; }
 int gemm_mode() { return g_opt_gemm_mode.load(); }
+bool stream_k_enabled() { return g_opt_stream_k.load() != 0; }
 
 }  // namespace bp
 
@@ -75,6 +76,7 @@ int bp_set_option(int option, int value) {
     case BP_OPT_ATTN_EXACT: bp::g_opt_attn_exact.store(value); return BP_OK;
     case BP_OPT_GEMM_SIMT: bp::g_opt_gemm_simt.store(value); return BP_OK;
     case BP_OPT_GEMM_MODE: bp::g_opt_gemm_mode.store(value); return BP_OK;
+    case BP_OPT_STREAM_K: bp::g_opt_stream_k.store(value); return BP_OK;
     default: bp::set_error("bp_set_option: unknown option %d", option); return BP_ERR_INVALID;
   }
 }

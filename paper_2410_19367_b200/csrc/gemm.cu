@@ -17,6 +17,7 @@
 #include "common.cuh"
 
 #include <mutex>
+#include <unordered_map>
 
 namespace bp {
 
@@ -344,27 +345,113 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 }
 
 
+// ============================================ stream-K work schedule ====
+// Tiles 0..dp-1 are handed out round-robin as whole tiles ("data
+// parallel"); the remaining tiles' k-blocks are split evenly over the P CTA
+// pairs ("stream-K"), so every pair gets the same number of k-blocks and
+// the last wave is no longer quantised to whole tiles.  A pair's stream-K
+// range covers at most one partial tile head (a "contributor" segment,
+// k-blocks [kb0, kb1) with kb1 < KB: its raw fp32 accumulator goes to the
+// pair's workspace slot and a flag is raised) and at most one partial tile
+// tail (an "owner" segment, kb1 == KB, kb0 > 0: it waits for the
+// contributors' flags and adds their partials before the epilogue).
+// Contributor segments run FIRST and owner segments LAST, so no pair ever
+// waits on a pair that is itself waiting.
+struct Seg {
+  int tile, kb0, kb1, role;  // role: 0 whole tile, 1 owner, 2 contributor
+};
+
+struct SkSched {
+  int T, KB, P, p, dp;
+  long U, lo, hi;
+  int nsk;
+  Seg sk[4];
+  int first_contrib;  // 1 if sk[0] is this pair's contributor segment (run first)
+
+  BP_DEV void init(int T_, int KB_, int P_, int p_, int enable) {
+    T = T_; KB = KB_; P = P_; p = p_;
+    dp = (!enable || T % P == 0) ? T : (T / P >= 1 ? (T / P - 1) * P : 0);
+    U = (long)(T - dp) * KB;
+    lo = U * p / P;
+    hi = U * (p + 1) / P;
+    nsk = 0;
+    Seg tmp[4];
+    int n = 0;
+    for (long u = lo; u < hi && n < 4;) {
+      const int rel = (int)(u / KB), kb0 = (int)(u % KB);
+      const long take = (hi - u) < (long)(KB - kb0) ? (hi - u) : (long)(KB - kb0);
+      const int kb1 = kb0 + (int)take;
+      const int role = (kb0 == 0 && kb1 == KB) ? 0 : (kb1 == KB ? 1 : 2);
+      tmp[n++] = Seg{dp + rel, kb0, kb1, role};
+      u += take;
+    }
+    first_contrib = (n > 0 && tmp[n - 1].role == 2) ? 1 : 0;
+    if (first_contrib) sk[nsk++] = tmp[n - 1];
+    for (int i = 0; i < n - first_contrib; ++i) sk[nsk++] = tmp[i];
+  }
+  BP_DEV int n_dp() const { return dp > p ? (dp - p + P - 1) / P : 0; }
+  BP_DEV int count() const { return n_dp() + nsk; }
+  // execution order: [contributor] [dp tiles] [owner / whole sk tiles]
+  BP_DEV Seg get(int i) const {
+    if (first_contrib) {
+      if (i == 0) return sk[0];
+      --i;
+      if (i < n_dp()) return Seg{p + i * P, 0, KB, 0};
+      return sk[1 + (i - n_dp())];
+    }
+    if (i < n_dp()) return Seg{p + i * P, 0, KB, 0};
+    return sk[i - n_dp()];
+  }
+  // pairs whose contributor segment belongs to SK tile `tile`: q in
+  // [q_lo, p) with hi_q strictly inside the tile's unit range
+  BP_DEV int contrib_lo(int tile) const {
+    const long ts = (long)(tile - dp) * KB;
+    int q = p;
+    while (q > 0 && U * q / P > ts) --q;  // hi_{q-1} = U*q/P
+    return q;
+  }
+};
+
+struct SkWs {
+  float* part;      // [P][2 CTAs][128][BN] fp32 partial accumulators
+  unsigned* flag;   // [P][2]
+  unsigned epoch;
+  int enable;
+};
+
+BP_DEV void flag_release(unsigned* f, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+BP_DEV unsigned flag_acquire(const unsigned* f) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  return v;
+}
+BP_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
 // ============================================ tcgen05 2-SM (CTA pair) ====
 // Pair tile 256 x 256: each CTA of the cluster holds 128 rows of A and 128
 // rows (N-half) of B per stage; the leader issues tcgen05.mma.cta_group::2
 // (M=256, N=256) reading both CTAs' smem, each CTA's TMEM receives its own
 // 128 x 256 accumulator.  Halves the per-SM operand traffic of the 1-SM
 // kernel (L2 -> SM bandwidth is the bound there).
-template <int BN_>
+template <int BN_, bool B_MN_>
 struct Tc2Cfg {
-  static constexpr int BM = 128, BN = BN_, BNH = BN_ / 2, BK = 64, STAGES = BN_ == 256 ? 6 : 8;
+  static constexpr int BM = 128, BN = BN_, BNH = BN_ / 2, BK = 64;
+  static constexpr int BCH = (BNH + 63) / 64;  // 64-wide chunks of an MN-major B half
   static constexpr uint32_t A_BYTES = BM * BK * 2;
-  static constexpr uint32_t B_BYTES = BNH * BK * 2;
+  static constexpr uint32_t B_BYTES = B_MN_ ? BCH * 64 * BK * 2 : BNH * BK * 2;
+  static constexpr int STAGES = (200 * 1024) / (A_BYTES + B_BYTES) > 8 ? 8 : (200 * 1024) / (A_BYTES + B_BYTES);
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static constexpr uint32_t TMEM_COLS = 2 * BN <= 256 ? 256 : 512;  // power of two
   static constexpr size_t SMEM = 1024 + STAGES * (size_t)STAGE_BYTES + 256;
 };
 
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                int M, int N, int K, Epi ep) {
-  using C = Tc2Cfg<BN>;
+                int M, int N, int K, Epi ep, SkWs ws) {
+  using C = Tc2Cfg<BN, B_MN>;
   constexpr int BK = C::BK, STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -383,6 +470,9 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   const int num_tiles = tiles_m * tiles_n;
   const int kblocks = (K + BK - 1) / BK;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  SkSched sch;
+  sch.init(num_tiles, kblocks, ncl, cid, ws.enable);
+  const int nseg = sch.count();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
@@ -409,10 +499,12 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     if (lane == 0) {  // -------------------------- TMA producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cid; tile < num_tiles; tile += ncl) {
+      for (int si = 0; si < nseg; ++si) {
+        const Seg sg = sch.get(si);
+        const int tile = sg.tile;
         const int m0 = (tile % tiles_m) * 256 + rank * 128;
         const int n0 = (tile / tiles_m) * C::BN + rank * C::BNH;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * C::A_BYTES;
           uint8_t* b = sB + stage * C::B_BYTES;
@@ -427,7 +519,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             tma_load_2d_2sm(b, &map_b, k0, n0, &full[stage]);
           } else {
 #pragma unroll
-            for (int c = 0; c < C::BNH / 64; ++c)
+            for (int c = 0; c < C::BCH; ++c)
               tma_load_2d_2sm(b + c * (BK * 128), &map_b, n0 + 64 * c, k0, &full[stage]);
           }
           if (leader)
@@ -444,13 +536,14 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
+      for (int si = 0; si < nseg; ++si, ++it) {
+        const Seg sg = sch.get(si);
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * C::BN;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
@@ -461,7 +554,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                                      : umma_desc_sw128(a_addr + k * 32, 0, 1024);
             const uint64_t bd = B_MN ? umma_desc_sw128(b_addr + k * 2048, BK * 128, 1024)
                                      : umma_desc_sw128(b_addr + k * 32, 0, 1024);
-            tc_mma_f16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            tc_mma_f16_2sm(d_tmem, ad, bd, idesc, (kb > sg.kb0) || (k != 0));
           }
           tc_commit_2sm_mc(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -472,7 +565,9 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   } else if (warp >= 4) {  // ---------------------- epilogue (both CTAs)
     const int ew = warp - 4;
     int it = 0;
-    for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
+    for (int si = 0; si < nseg; ++si, ++it) {
+      const Seg sg = sch.get(si);
+      const int tile = sg.tile;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int m0 = (tile % tiles_m) * 256 + rank * 128;
@@ -480,8 +575,46 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = m0 + ew * 32 + lane;
+      const int lrow = ew * 32 + lane;  // row within this CTA's half tile
       const uint32_t t0 = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * C::BN;
-      epi_tile<C::BN / 32>(ep, t0, row, n0);
+      if (sg.role == 2) {
+        // contributor: raw fp32 partial -> workspace slot, then publish
+        float* dst = ws.part + (((size_t)cid * 2 + rank) * 128 + lrow) * C::BN;
+#pragma unroll 1
+        for (int c = 0; c < C::BN / 32; ++c) {
+          float v[32];
+          tmem_ld_32x32b_x32(t0 + c * 32, v);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            reinterpret_cast<float4*>(dst + c * 32)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+        __threadfence();
+        epi_bar();
+        if (ew == 0 && lane == 0) flag_release(&ws.flag[cid * 2 + rank], ws.epoch);
+      } else if (sg.role == 1) {
+        // owner: wait for every contributor of this tile, add partials
+        const int qlo = sch.contrib_lo(tile);
+        for (int q = qlo; q < cid; ++q)
+          while (flag_acquire(&ws.flag[q * 2 + rank]) != ws.epoch) {
+          }
+#pragma unroll 1
+        for (int c = 0; c < C::BN / 32; ++c) {
+          float v[32];
+          tmem_ld_32x32b_x32(t0 + c * 32, v);
+          for (int q = qlo; q < cid; ++q) {
+            const float4* src =
+                reinterpret_cast<const float4*>(ws.part + (((size_t)q * 2 + rank) * 128 + lrow) * C::BN + c * 32);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 t = __ldcg(src + i);
+              v[4 * i] += t.x; v[4 * i + 1] += t.y; v[4 * i + 2] += t.z; v[4 * i + 3] += t.w;
+            }
+          }
+          if (n0 + c * 32 < N) epi_row32(ep, row, n0 + c * 32, v);
+        }
+      } else {
+        epi_tile<C::BN / 32>(ep, t0, row, n0);
+      }
       tc_fence_before();
       if (leader)
         mbar_arrive(&tempty[acc]);
@@ -631,9 +764,48 @@ static int dispatch_tc(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
 }
 
 
+
+// Per-stream stream-K workspace (partials + flags).  Concurrent GEMMs on
+// different streams never share a slot; the epoch makes flags self-resetting.
+struct SkWsState {
+  float* part = nullptr;
+  size_t part_floats = 0;
+  unsigned* flag = nullptr;
+  int nflag = 0;
+  unsigned epoch = 0;
+};
+static std::mutex g_sk_mu;
+static std::unordered_map<uint64_t, SkWsState> g_sk;
+
+bool stream_k_enabled();
+
+static int sk_workspace(cudaStream_t st, size_t floats, int nflag, SkWs* out) {
+  int dev = 0;
+  BP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_sk_mu);
+  SkWsState& w = g_sk[(reinterpret_cast<uint64_t>(st) << 4) ^ (uint64_t)dev];
+  if (w.part_floats < floats) {
+    if (w.part) BP_CUDA(cudaFree(w.part));
+    BP_CUDA(cudaMalloc(&w.part, floats * sizeof(float)));
+    w.part_floats = floats;
+  }
+  if (w.nflag < nflag) {
+    if (w.flag) BP_CUDA(cudaFree(w.flag));
+    BP_CUDA(cudaMalloc(&w.flag, nflag * sizeof(unsigned)));
+    BP_CUDA(cudaMemset(w.flag, 0, nflag * sizeof(unsigned)));
+    w.nflag = nflag;
+  }
+  ++w.epoch;
+  if (w.epoch == 0) w.epoch = 1;
+  out->part = w.part;
+  out->flag = w.flag;
+  out->epoch = w.epoch;
+  return BP_OK;
+}
+
 template <int BN, bool A_MN, bool B_MN>
 static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
-  using C = Tc2Cfg<BN>;
+  using C = Tc2Cfg<BN, B_MN>;
   CUtensorMap ma, mb;
   int rc;
   if (!A_MN)
@@ -654,8 +826,13 @@ static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   }
   const int tiles = ((g.M + 255) / 256) * ((g.N + C::BN - 1) / C::BN);
   const int pairs = num_sms() / 2;
-  const int grid = 2 * (tiles < pairs ? tiles : pairs);
-  kern<<<grid, 256, C::SMEM, st>>>(ma, mb, g.M, g.N, g.K, ep);
+  const int npairs = tiles < pairs ? tiles : pairs;
+  SkWs ws{};
+  ws.enable = (stream_k_enabled() && tiles > npairs && tiles % npairs != 0) ? 1 : 0;
+  if (ws.enable) {
+    if (int rc = sk_workspace(st, (size_t)npairs * 2 * 128 * C::BN, npairs * 2, &ws)) return rc;
+  }
+  kern<<<2 * npairs, 256, C::SMEM, st>>>(ma, mb, g.M, g.N, g.K, ep, ws);
   count_launch();
   BP_CHECK_LAUNCH("gemm_tc2");
   return BP_OK;
@@ -670,14 +847,40 @@ static int dispatch_tc2_bn(const bp_gemm_args& g, const Epi& ep, cudaStream_t st
   return launch_tc2<BN, true, true>(g, ep, st);
 }
 
-// Pair tile 256 x 256 unless that leaves the GPU under one wave of pairs,
-// then 256 x 128 (twice the tiles, so each pair overlaps one tile's
-// epilogue with the next tile's MMAs).
+// Pair-tile width BN in {256, 224, 192, 128}.  Per k-block a CTA streams
+// 16 KB of A plus BN/2 x 128 B of B from L2, so narrower tiles move more
+// bytes per FLOP (measured: BN=128 runs 30% slower per FLOP than 256).
+// Model the time of a launch as rounds(BN) * (128 + BN/2) -- the wave
+// quantisation over 74 CTA pairs times the per-tile operand traffic -- and
+// pick the minimum (N = 8192 at M = 2048: 224 gives exactly 4 waves).
+int pick_tc2_bn(int M, int N, int pairs, bool b_mn_major) {
+  static const int cand[4] = {256, 224, 192, 128};
+  const int tm = (M + 255) / 256;
+  int best = 256;
+  long best_score = -1;
+  for (int i = 0; i < 4; ++i) {
+    const int bn = cand[i];
+    // an MN-major B half of 112 / 96 columns still loads two full 64-wide
+    // TMA boxes; measured slower than 256, so only K-major B narrows
+    if (b_mn_major && (bn == 224 || bn == 192)) continue;
+    const long tiles = (long)tm * ((N + bn - 1) / bn);
+    const long rounds = (tiles + pairs - 1) / pairs;
+    const long score = rounds * (128 + bn / 2);
+    if (best_score < 0 || score < best_score) {
+      best_score = score;
+      best = bn;
+    }
+  }
+  return best;
+}
+
 static int dispatch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
-  const int pairs = num_sms() / 2;
-  const int t256 = ((g.M + 255) / 256) * ((g.N + 255) / 256);
-  if (t256 < pairs && g.N >= 128) return dispatch_tc2_bn<128>(g, ep, st);
-  return dispatch_tc2_bn<256>(g, ep, st);
+  switch (pick_tc2_bn(g.M, g.N, num_sms() / 2, !g.b_kmajor)) {
+    case 224: return dispatch_tc2_bn<224>(g, ep, st);
+    case 192: return dispatch_tc2_bn<192>(g, ep, st);
+    case 128: return dispatch_tc2_bn<128>(g, ep, st);
+    default: return dispatch_tc2_bn<256>(g, ep, st);
+  }
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }

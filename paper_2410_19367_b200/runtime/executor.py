@@ -314,6 +314,60 @@ class Trainer:
                 out.setdefault(n, t.detach().float().cpu().clone())
         return out
 
+    def measure_task_times(self, reps: int = 3) -> dict:
+        """Isolated device time (ms) of every distinct task class of this
+        schedule: {(direction, stage, 'F'|'B'): ms}, each timed alone on one
+        stream with CUDA events (median of ``reps``) on synthetic inputs."""
+        cfg = self.cfg
+        M = cfg.micro_batch * cfg.seq
+        dev = self.device
+        st = torch.cuda.Stream(device=dev)
+        tok = torch.randint(0, cfg.vocab, (M,), device=dev, dtype=torch.int32)
+        loss = torch.zeros(1, device=dev)
+        d0 = self.local_devices[0]
+        out = {}
+        torch.cuda.synchronize(dev)
+        for (dr, s), comp in self.compute.items():
+            ft, bt = [], []
+            for _ in range(reps + 1):
+                x0 = None if s == 0 else (torch.randn(M, cfg.hidden, device=dev) * 0.1).to(self.dtype)
+                dy = None if s == self.S - 1 else (torch.randn(M, cfg.hidden, device=dev) * 1e-3).to(self.dtype)
+                torch.cuda.synchronize(dev)
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0.record(st)
+                stash, msg = comp.forward(st, self.pool, x0=x0, tokens=tok, targets=tok, loss_slot=loss)
+                e1.record(st)
+                dx, release = comp.backward(st, self.pool, stash, dy, self.ws[d0])
+                e2.record(st)
+                torch.cuda.synchronize(dev)
+                ft.append(e0.elapsed_time(e1))
+                bt.append(e1.elapsed_time(e2))
+                ev = torch.cuda.Event()
+                ev.record(st)
+                self.pool.put_all([t for t in release if t is not None] + [msg, dx], ev)
+            out[(dr, s, "F")] = sorted(ft[1:])[len(ft[1:]) // 2]
+            out[(dr, s, "B")] = sorted(bt[1:])[len(bt[1:]) // 2]
+        for sp in self.stage_params.values():
+            sp.grad.zero_()
+        return out
+
+    def replay_bubble(self, times: dict) -> dict:
+        """ASAP replay (reference ``list_schedule``, fusion.py:34-77) of the
+        executed per-device orders with the MEASURED task times: the makespan
+        and bubble the schedule would have with one GPU per logical device and
+        free communication (SPEC.md:263 bubble definition)."""
+        from fractions import Fraction
+        from ..schedule import list_schedule
+        us = {k: Fraction(round(v * 1000)) for k, v in times.items()}   # integer microseconds
+        def dur(t):
+            return us[(t.direction, t.stage, t.kind.value)]
+        starts = list_schedule(self.sched.per_device, self.sched.dependencies, dur)
+        mk = max(st + dur(t) for t, st in starts.items())
+        busy = [sum(dur(t) for t in row) for row in self.sched.per_device]
+        beta = 1 - Fraction(sum(busy)) / (self.D * mk)
+        return {"makespan_ms": float(mk) / 1000, "bubble": float(beta),
+                "busy_ms_per_device": [float(b) / 1000 for b in busy]}
+
     def measured_bubble(self):
         """Per-device busy time / makespan from the last step's per-task CUDA
         events and beta = 1 - sum busy / (D * makespan).

@@ -11,13 +11,14 @@ import os
 import threading
 
 __all__ = ["lib", "GemmArgs", "check", "LIB_PATH", "BP_F32", "BP_BF16", "EPI_NONE", "EPI_GELU", "EPI_DGELU",
-           "OPT_ATTN_EXACT", "OPT_GEMM_SIMT", "OPT_GEMM_MODE"]
+           "OPT_ATTN_EXACT", "OPT_GEMM_SIMT", "OPT_GEMM_MODE",
+           "OPT_STREAM_K"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "libbitpipe_b200.so")
 
 BP_F32, BP_BF16 = 0, 1
 EPI_NONE, EPI_GELU, EPI_DGELU = 0, 1, 2
-OPT_ATTN_EXACT, OPT_GEMM_SIMT, OPT_GEMM_MODE = 1, 2, 3
+OPT_ATTN_EXACT, OPT_GEMM_SIMT, OPT_GEMM_MODE, OPT_STREAM_K = 1, 2, 3, 4
 ABI_VERSION = 1
 
 _vp = ctypes.c_void_p

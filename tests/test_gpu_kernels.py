@@ -27,7 +27,7 @@ def _seed():
 
 
 SHAPES = [(128, 128, 64), (256, 512, 128), (300, 200, 192), (2048, 6144, 2048), (384, 2304, 1024),
-          (512, 50304 // 8, 256), (130, 136, 72)]
+          (512, 50304 // 8, 256), (130, 136, 72), (2048, 8192, 256), (8192, 2048, 128), (2048, 1000, 64)]
 
 
 @pytest.fixture(params=[1, 2], ids=["1sm", "2sm"])
@@ -266,3 +266,29 @@ def test_flash_matches_exact_path(S, Dh, causal):
     for part in range(3):   # q, k, v gradient blocks separately
         sl = slice(part * hd, (part + 1) * hd)
         assert _relerr(d0[:, sl], d2[:, sl]) < 2e-2, part
+
+
+@pytest.mark.parametrize("M,N,K,ak,bk,acc", [(2048, 6144, 512, True, True, False), (8192, 2048, 256, False, False, True),
+                                            (4096, 3072, 320, True, False, False), (2304, 2304, 1024, True, True, True)])
+def test_gemm_stream_k_matches_data_parallel(M, N, K, ak, bk, acc):
+    """Stream-K tail split (owner/contributor fix-up) == whole-tile schedule."""
+    from paper_2410_19367_b200.runtime.lib import OPT_STREAM_K
+    A = (torch.randn(M, K) if ak else torch.randn(K, M)).cuda().bfloat16()
+    B = (torch.randn(N, K) if bk else torch.randn(K, N)).cuda().bfloat16()
+    base = torch.randn(M, N, device="cuda")
+    outs = []
+    for skv in (1, 0):
+        ops.set_option(OPT_STREAM_K, skv)   # default is 0; force the stream-K path on
+        try:
+            C = base.clone() if acc else torch.empty(M, N, device="cuda")
+            for _ in range(2):   # second launch exercises the epoch-based flag reuse
+                C2 = base.clone() if acc else C
+                ops.gemm(A, B, C2, a_kmajor=ak, b_kmajor=bk, beta=1.0 if acc else 0.0)
+            torch.cuda.synchronize()
+            outs.append(C2)
+        finally:
+            ops.set_option(OPT_STREAM_K, 0)
+    opA = A.float() if ak else A.float().t()
+    opB = B.float().t() if bk else B.float()
+    ref = opA @ opB + (base if acc else 0)
+    assert _relerr(outs[0], ref) < 1e-5 and _relerr(outs[1], ref) < 1e-5

@@ -76,14 +76,16 @@ def run_pair(label, text, cfg_name, dtype, tol_loss, tol_grad, check_params):
         gd = tr.gather("grads", ps.Direction.DOWN)
         gu = tr.gather("grads", ps.Direction.UP)
         grads = {k: 0.5 * (gd[k] + gu[k]) for k in gd}
-    worst = max(rel(grads[k], ref.grads[k]) for k in ref.grads)
-    assert worst < tol_grad, worst
+    errs = {k: rel(grads[k], ref.grads[k]) for k in ref.grads}
+    wk = max(errs, key=errs.get)
+    assert errs[wk] < tol_grad, (wk, errs[wk], ref.grads[wk].norm().item())
     if check_params:
         master = tr.gather("master")
         upd_ours = {k: master[k] - params[k] for k in params}
         upd_ref = {k: ref.params[k] - params[k].double() for k in params}
-        werr = max(rel(upd_ours[k], upd_ref[k]) for k in params)
-        assert werr < check_params, werr
+        werrs = {k: rel(upd_ours[k], upd_ref[k]) for k in params}
+        wk = max(werrs, key=werrs.get)
+        assert werrs[wk] < check_params, (wk, werrs[wk])
         # both replicas hold bit-identical working weights after the update
         if sched.is_bidirectional:
             pd = tr.gather("params", ps.Direction.DOWN)
