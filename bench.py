@@ -33,6 +33,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "GPT tokens/sec/box at D=1/2/4/8 B200 (frac of roofline); bubble fraction"
+# ncu --set full, fc1 forward GEMM 2048x8192x2048 (profiles/r1_ncu_full_summary.txt):
+# dram__bytes_read.sum + dram__bytes_write.sum per launch
+TRAFFIC_FC1_BYTES = 42.026496e6 + 2.713344e6
 
 
 def parse():
@@ -248,25 +251,31 @@ def main():
     beta_ideal = float(ps.analytic_bubble_ratio(approach, D, N)) if G > 1 else 0.0
     roof_tps = G * peak_sust * 1e12 * (1 - beta_ideal) / F_tok
     beta_order = float(ps.canonical_bubble(sched))
-    # dominant kernel: MLP fc1 forward GEMM of one micro-batch (M=B*S, N=4h, K=h), timed live
+    # dominant kernel: the tcgen05 GEMM.  Live: CUDA events around every GEMM
+    # launch (on its own stream) during one extra step after the timed region,
+    # with the logical devices' work serialised on one stream so that a
+    # launch's span is its own device time (in the concurrent step the spans
+    # overlap other streams' kernels).  Serialised step time is reported too.
     Mtok = cfg.micro_batch * cfg.seq
-    A = torch.randn(Mtok, cfg.hidden, device="cuda").bfloat16()
-    W = torch.randn(cfg.ffn, cfg.hidden, device="cuda").bfloat16()
-    C = torch.empty(Mtok, cfg.ffn, device="cuda", dtype=torch.bfloat16)
-    for _ in range(5):
-        ops.gemm(A, W, C)
+    if world == 1:
+        tr.streams = {d: main_stream for d in tr.streams}
+    tr.train_step(tok_d, tgt_d)
     torch.cuda.synchronize()
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 50
-    k0.record(main_stream)
-    for _ in range(reps):
-        ops.gemm(A, W, C)
-    k1.record(main_stream)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ops.gemm_probe_start()
+    s0.record(main_stream)
+    tr.train_step(tok_d, tgt_d)
+    s1.record(main_stream)
     torch.cuda.synchronize()
-    gemm_ms = k0.elapsed_time(k1) / reps
-    gemm_flops = 2.0 * Mtok * cfg.ffn * cfg.hidden
-    achieved = gemm_flops / (gemm_ms / 1e3) / 1e12
-    del A, W, C
+    probes = ops.gemm_probe_stop()
+    serial_ms = s0.elapsed_time(s1)
+    gemm_flops = sum(p[0] for p in probes)
+    gemm_ms = sum(p[2].elapsed_time(p[3]) for p in probes)
+    n_gemm = len(probes)
+    achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+    gemm_share = gemm_ms / serial_ms if serial_ms > 0 else 0.0
+    fc1 = [p for p in probes if p[1] == (Mtok, cfg.ffn, cfg.hidden)]
+    fc1_us = 1e3 * sum(p[2].elapsed_time(p[3]) for p in fc1) / max(1, len(fc1))
 
     if rank == 0:
         clocks = clk.summary()
@@ -283,10 +292,18 @@ def main():
                        "l2": "working set (2.6 GB weights, GBs of activations) >> 126 MB L2"},
             "loss_mean": loss_mean,
             "e2e": e2e,
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s",
-                         "frac": achieved / peak_burst, "traffic": None,
-                         "kernel": f"bp gemm_tc fc1 fprop {Mtok}x{cfg.ffn}x{cfg.hidden} bf16",
-                         "peak_kind": peak_kind},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_sust, "unit": "TFLOP/s",
+                         "frac": achieved / peak_sust,
+                         "traffic": TRAFFIC_FC1_BYTES,
+                         "kernel": "bp::gemm_tc2_kernel (tcgen05 2-SM GEMM), all launches of one step "
+                                   "(logical devices serialised on one stream, events per launch)",
+                         "serial_step_ms": serial_ms,
+                         "launches": n_gemm, "avg_launch_us": 1e3 * gemm_ms / max(1, n_gemm),
+                         "algorithmic_flops_per_launch": gemm_flops / max(1, n_gemm),
+                         "share_of_step": gemm_share, "fc1_fprop_avg_us": fc1_us,
+                         "peak_kind": f"{peak_kind} sustained (kernel timed inside a long step)",
+                         "traffic_note": "dram read+write bytes per fc1-fprop launch from ncu --set full "
+                                         "(profiles/r1_ncu_full_summary.txt)"},
             "step_roofline": {"tokens_per_s": roof_tps, "frac": value / roof_tps, "F_tok": F_tok,
                               "peak_tflops": peak_sust, "peak_kind": f"{peak_kind} sustained",
                               "beta_ideal": beta_ideal, "model_tflops": value * F_tok / 1e12},

@@ -76,7 +76,9 @@ BP_API int bp_set_option(int option, int value);
  *   b_kmajor = 1 : B stored [N,K] (row-major, ldb >= K)   ("x W^T")
  *   b_kmajor = 0 : B stored [K,N] (row-major, ldb >= N)
  * in_dtype BP_BF16 runs the tcgen05/TMEM/TMA tensor-core kernel (fp32
- * accumulate); BP_F32 runs an exact-fp32 SIMT kernel (check mode, no TF32).
+ * accumulate) whenever A/B have 16-byte aligned bases and row pitches
+ * (else the SIMT kernel); BP_F32 runs an exact-fp32 SIMT kernel (check
+ * mode, no TF32).
  * beta must be 0 or 1; beta = 1 accumulates into C (C must be fp32).
  * bias: [N] in in_dtype or NULL.  residual: [M,N] in c_dtype or NULL.
  * aux : [M,N] in c_dtype (GELU pre-activation) for BP_EPI_GELU/DGELU.

@@ -916,12 +916,10 @@ extern "C" int bp_gemm(const bp_gemm_args* gp, void* stream) {
   ep.vec_ok = aligned16(g.C) && (g.ldc * esz) % 16 == 0 && (!g.bias || aligned16(g.bias)) &&
               (!g.residual || (aligned16(g.residual) && (g.ldr * esz) % 16 == 0)) &&
               (!g.aux || (aligned16(g.aux) && (g.ldaux * esz) % 16 == 0));
-  if (g.in_dtype == BP_BF16 && !g.force_simt && !opt_gemm_simt()) {
-    const bool ok = aligned16(g.A) && aligned16(g.B) && (g.lda % 8) == 0 && (g.ldb % 8) == 0;
-    if (!ok) {
-      set_error("bp_gemm: bf16 operands need 16-byte aligned bases and ld %% 8 == 0");
-      return BP_ERR_INVALID;
-    }
+  // TMA needs 16-byte aligned bases and row pitches; other bf16 operands
+  // (e.g. a vocabulary that is not a multiple of 8) take the SIMT kernel.
+  const bool tma_ok = aligned16(g.A) && aligned16(g.B) && (g.lda % 8) == 0 && (g.ldb % 8) == 0;
+  if (g.in_dtype == BP_BF16 && !g.force_simt && !opt_gemm_simt() && tma_ok) {
     const int mode = gemm_mode();
     if (mode == 2 || (mode == 0 && g.M >= 256 && g.N >= 256)) return dispatch_tc2(g, ep, st);
     const int tiles256 = ((g.M + 127) / 128) * ((g.N + 255) / 256);

@@ -70,7 +70,7 @@ CONFIGS = {
     "gpt-10b": ModelConfig("gpt-10b", layers=48, hidden=4096, heads=32, seq=2048, vocab=50304, micro_batch=1),
     # small configs used by tests
     "small": ModelConfig("small-gpt", layers=4, hidden=256, heads=4, seq=128, vocab=512, micro_batch=2),
-    "small-bert": ModelConfig("small-bert", layers=2, hidden=128, heads=2, seq=64, vocab=300, micro_batch=2,
+    "small-bert": ModelConfig("small-bert", layers=2, hidden=128, heads=2, seq=128, vocab=300, micro_batch=2,
                               causal=False),
 }
 

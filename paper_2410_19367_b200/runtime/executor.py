@@ -106,7 +106,8 @@ class Trainer:
     """
 
     def __init__(self, cfg: ModelConfig, schedule: Schedule, *, dtype=torch.bfloat16, optim: OptimConfig | None = None,
-                 params: dict | None = None, seed: int = 1234, device=None, dist_ctx=None, record_timeline=False):
+                 params: dict | None = None, seed: int = 1234, device=None, dist_ctx=None, record_timeline=False,
+                 serial_streams: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("BitPipe Trainer needs a CUDA device (no CPU fallback)")
         ops.lib()  # fail loudly now if the kernel library is missing
@@ -154,7 +155,11 @@ class Trainer:
         del params
 
         # -- streams, pools, workspaces ------------------------------------------------
-        self.streams = {d: torch.cuda.Stream(device=self.device) for d in self.local_devices}
+        if serial_streams:   # all logical devices on one stream (no cross-device kernel concurrency)
+            one = torch.cuda.Stream(device=self.device)
+            self.streams = {d: one for d in self.local_devices}
+        else:
+            self.streams = {d: torch.cuda.Stream(device=self.device) for d in self.local_devices}
         self.opt_stream = torch.cuda.Stream(device=self.device)
         self.pool = BufferPool(self.device)
         wsn = ops.attn_workspace_numel(cfg.micro_batch, cfg.seq, cfg.heads, cfg.head_dim)

@@ -43,6 +43,23 @@ def _rowmajor(t: torch.Tensor, name: str) -> None:
         raise ValueError(f"{name} must be a CUDA tensor")
 
 
+# Optional live probe of the tensor-core GEMM launches (bench.py): CUDA
+# events recorded on the launching stream around every bf16 bp_gemm call.
+_gemm_probe = None
+
+
+def gemm_probe_start() -> None:
+    global _gemm_probe
+    _gemm_probe = []
+
+
+def gemm_probe_stop():
+    """Returns [(flops, shape, start_event, end_event)] of the probed launches."""
+    global _gemm_probe
+    out, _gemm_probe = _gemm_probe, None
+    return out or []
+
+
 def set_option(option: int, value: int) -> None:
     check(lib().bp_set_option(option, int(value)), "bp_set_option")
 
@@ -79,7 +96,15 @@ def gemm(a, b, c, *, a_kmajor=True, b_kmajor=True, alpha=1.0, beta=0.0, bias=Non
         g.aux, g.ldaux = aux.data_ptr(), aux.stride(0)
     g.epilogue = int(epilogue)
     g.force_simt = int(bool(force_simt))
+    probe = _gemm_probe is not None and g.in_dtype == BP_BF16
+    if probe:
+        st = stream if stream is not None else torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
     check(lib().bp_gemm(ctypes.byref(g), _s(stream)), "bp_gemm")
+    if probe:
+        e1.record(st)
+        _gemm_probe.append((2.0 * M * N * K, (int(M), int(N), int(K)), e0, e1))
 
 
 def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):

@@ -41,9 +41,7 @@ def gemm_mode(request):
 @pytest.mark.parametrize("M,N,K", SHAPES)
 @pytest.mark.parametrize("ak,bk", [(True, True), (True, False), (False, False), (False, True)])
 def test_gemm_bf16_tc(M, N, K, ak, bk, gemm_mode):
-    if (not ak and M % 8) or (not bk and N % 8) or K % 8:
-        pytest.skip("TMA needs 16-byte row pitches")
-    dev = "cuda"
+    dev = "cuda"   # shapes without 16-byte row pitches take the SIMT kernel
     A = torch.randn(M, K, device=dev) if ak else torch.randn(K, M, device=dev)
     B = torch.randn(N, K, device=dev) if bk else torch.randn(K, N, device=dev)
     A16, B16 = A.bfloat16(), B.bfloat16()

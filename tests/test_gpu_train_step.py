@@ -105,3 +105,16 @@ def test_fp32_check_mode_tiny(label):
 def test_bf16_small(label):
     text = golden()[label]
     run_pair(label, text, "small", torch.bfloat16, 2e-2, 2e-2, check_params=None)
+
+
+@pytest.mark.parametrize("label", ["D=4;N=8;approach=bitpipe;v=2", "D=4;N=4;approach=chimera"])
+def test_bf16_small_bert_bidirectional_attention(label):
+    """BERT-style (non-causal attention, head_dim 64) through the tcgen05
+    attention kernels and the same executor."""
+    text = golden()[label]
+    run_pair(label, text, "small-bert", torch.bfloat16, 2e-2, 2e-2, check_params=None)
+
+
+def test_fp32_small_bert_check_mode():
+    label = "D=4;N=8;approach=bitpipe;v=2"
+    run_pair(label, golden()[label], "small-bert", torch.float32, 1e-4, 1e-4, check_params=1e-3)
