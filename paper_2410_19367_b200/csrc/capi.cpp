@@ -44,7 +44,7 @@ bool opt_attn_exact() { return g_opt_attn_exact.load() == 1; }
 bool opt_attn_no_tc() { return g_opt_attn_exact.load() != 0; }
 bool opt_gemm_simt() { return g_opt_gemm_simt.load() != 0; }
 int gemm_mode() { return g_opt_gemm_mode.load(); }
-bool stream_k_enabled() { return g_opt_stream_k.load() != 0; }
+int stream_k_mode() { return g_opt_stream_k.load(); }
 
 }  // namespace bp
 

@@ -597,19 +597,31 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         for (int q = qlo; q < cid; ++q)
           while (flag_acquire(&ws.flag[q * 2 + rank]) != ws.epoch) {
           }
-#pragma unroll 1
-        for (int c = 0; c < C::BN / 32; ++c) {
-          float v[32];
-          tmem_ld_32x32b_x32(t0 + c * 32, v);
+        // partial sum of all contributors for chunk c, one chunk of lookahead
+        auto load_part = [&](int c, float (&acc)[32]) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[i] = 0.f;
           for (int q = qlo; q < cid; ++q) {
             const float4* src =
                 reinterpret_cast<const float4*>(ws.part + (((size_t)q * 2 + rank) * 128 + lrow) * C::BN + c * 32);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const float4 t = __ldcg(src + i);
-              v[4 * i] += t.x; v[4 * i + 1] += t.y; v[4 * i + 2] += t.z; v[4 * i + 3] += t.w;
+              acc[4 * i] += t.x; acc[4 * i + 1] += t.y; acc[4 * i + 2] += t.z; acc[4 * i + 3] += t.w;
             }
           }
+        };
+        float nxt[32];
+        load_part(0, nxt);
+#pragma unroll 1
+        for (int c = 0; c < C::BN / 32; ++c) {
+          float v[32], cur[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) cur[i] = nxt[i];
+          if (c + 1 < C::BN / 32) load_part(c + 1, nxt);
+          tmem_ld_32x32b_x32(t0 + c * 32, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += cur[i];
           if (n0 + c * 32 < N) epi_row32(ep, row, n0 + c * 32, v);
         }
       } else {
@@ -777,7 +789,7 @@ struct SkWsState {
 static std::mutex g_sk_mu;
 static std::unordered_map<uint64_t, SkWsState> g_sk;
 
-bool stream_k_enabled();
+int stream_k_mode();
 
 static int sk_workspace(cudaStream_t st, size_t floats, int nflag, SkWs* out) {
   int dev = 0;
@@ -826,9 +838,16 @@ static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   }
   const int tiles = ((g.M + 255) / 256) * ((g.N + C::BN - 1) / C::BN);
   const int pairs = num_sms() / 2;
-  const int npairs = tiles < pairs ? tiles : pairs;
+  int npairs = tiles < pairs ? tiles : pairs;
   SkWs ws{};
-  ws.enable = (stream_k_enabled() && tiles > npairs && tiles % npairs != 0) ? 1 : 0;
+  // stream-K: mode 1 = wherever the last wave is ragged; mode 0 (auto) =
+  // only sub-wave GEMMs with a long K (>= 64 k-blocks, e.g. the K = 8192
+  // MLP-down / LM-head dgrad shapes), which then use all pairs.
+  const int skm = stream_k_mode();
+  const int kb = (g.K + 63) / 64;
+  const bool sk_sub = skm != 2 && tiles < pairs && kb >= 64 && tiles * 2 > pairs;
+  if (sk_sub) npairs = pairs;
+  ws.enable = (sk_sub || (skm == 1 && tiles > npairs && tiles % npairs != 0)) ? 1 : 0;
   if (ws.enable) {
     if (int rc = sk_workspace(st, (size_t)npairs * 2 * 128 * C::BN, npairs * 2, &ws)) return rc;
   }

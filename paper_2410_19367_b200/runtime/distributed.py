@@ -82,6 +82,32 @@ class DistContext:
             for s in range(sched.num_stages):
                 a, b = dn.device_of(s), up.device_of(s)
                 self.pair_group[s] = (a, b, dist.new_group(sorted({a, b})))
+        self.warmup()
+
+    def warmup(self) -> None:
+        """Create every communicator up front, in one global order.
+
+        NCCL communicators (and torch's per-pair P2P communicators) are
+        created lazily by the first operation, and creation blocks until
+        both members arrive.  Posting all receives at iteration start could
+        then deadlock (rank a initialising link b->a while rank b
+        initialises link a->b).  Walking all groups in the same sorted
+        order with a blocking 1-element op makes creation deadlock-free.
+        """
+        dev = torch.device("cuda", torch.cuda.current_device()) if self.cuda else torch.device("cpu")
+        t = torch.zeros(1, device=dev)
+        for (src, dst) in sorted(self.link_group):
+            g = self.link_group[(src, dst)]
+            if self.rank == src:
+                dist.send(t, dst, group=g)
+            elif self.rank == dst:
+                dist.recv(t, src, group=g)
+        for s in sorted(self.pair_group):
+            a, b, g = self.pair_group[s]
+            if self.rank in (a, b):
+                dist.all_reduce(t, group=g)
+        if self.cuda:
+            torch.cuda.synchronize()
 
     # ------------------------------------------------------- primitives --
     def _sctx(self, stream):

@@ -267,7 +267,8 @@ def test_flash_matches_exact_path(S, Dh, causal):
 
 
 @pytest.mark.parametrize("M,N,K,ak,bk,acc", [(2048, 6144, 512, True, True, False), (8192, 2048, 256, False, False, True),
-                                            (4096, 3072, 320, True, False, False), (2304, 2304, 1024, True, True, True)])
+                                            (4096, 3072, 320, True, False, False), (2304, 2304, 1024, True, True, True),
+                                            (2048, 2048, 8192, True, False, False), (2048, 2048, 6144, True, True, True)])
 def test_gemm_stream_k_matches_data_parallel(M, N, K, ak, bk, acc):
     """Stream-K tail split (owner/contributor fix-up) == whole-tile schedule."""
     from paper_2410_19367_b200.runtime.lib import OPT_STREAM_K
@@ -275,8 +276,8 @@ def test_gemm_stream_k_matches_data_parallel(M, N, K, ak, bk, acc):
     B = (torch.randn(N, K) if bk else torch.randn(K, N)).cuda().bfloat16()
     base = torch.randn(M, N, device="cuda")
     outs = []
-    for skv in (1, 0):
-        ops.set_option(OPT_STREAM_K, skv)   # default is 0; force the stream-K path on
+    for skv in (1, 2):
+        ops.set_option(OPT_STREAM_K, skv)   # 1: force stream-K where ragged, 2: off
         try:
             C = base.clone() if acc else torch.empty(M, N, device="cuda")
             for _ in range(2):   # second launch exercises the epoch-based flag reuse
