@@ -64,8 +64,11 @@ enum bp_option {
                             > exact), 1 exact kernel, 2 mma.sync flash       */
   BP_OPT_GEMM_SIMT = 2,  /* 1: SIMT GEMM for bf16 too                          */
   BP_OPT_GEMM_MODE = 3,  /* tcgen05 tiling: 0 auto, 1 single-SM, 2 CTA pair    */
-  BP_OPT_STREAM_K = 4    /* stream-K GEMM scheduling: 0 auto (sub-wave, K >= 4096
-                            only), 1 every ragged last wave, 2 off           */
+  BP_OPT_STREAM_K = 4,   /* stream-K GEMM scheduling: 0 auto (sub-wave, K >= 4096
+                            only), 1 every ragged last wave, 2 off (default:
+                            measured slower on the GPT-1.3B shapes)          */
+  BP_OPT_GEMM_WIDE = 5   /* 256 x 512 pair tiles: 1 force (default 0: never,
+                            measured slower than 256 x 256)                  */
 };
 BP_API int bp_set_option(int option, int value);
 

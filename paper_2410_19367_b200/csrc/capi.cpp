@@ -12,7 +12,7 @@ namespace bp {
 
 static thread_local char g_err[1024] = "";
 static std::atomic<unsigned long long> g_launches{0};
-static std::atomic<int> g_opt_attn_exact{0}, g_opt_gemm_simt{0}, g_opt_gemm_mode{0}, g_opt_stream_k{0};
+static std::atomic<int> g_opt_attn_exact{0}, g_opt_gemm_simt{0}, g_opt_gemm_mode{0}, g_opt_stream_k{2}, g_opt_gemm_wide{0};
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -45,6 +45,7 @@ bool opt_attn_no_tc() { return g_opt_attn_exact.load() != 0; }
 bool opt_gemm_simt() { return g_opt_gemm_simt.load() != 0; }
 int gemm_mode() { return g_opt_gemm_mode.load(); }
 int stream_k_mode() { return g_opt_stream_k.load(); }
+int gemm_wide_mode() { return g_opt_gemm_wide.load(); }
 
 }  // namespace bp
 
@@ -77,6 +78,7 @@ int bp_set_option(int option, int value) {
     case BP_OPT_GEMM_SIMT: bp::g_opt_gemm_simt.store(value); return BP_OK;
     case BP_OPT_GEMM_MODE: bp::g_opt_gemm_mode.store(value); return BP_OK;
     case BP_OPT_STREAM_K: bp::g_opt_stream_k.store(value); return BP_OK;
+    case BP_OPT_GEMM_WIDE: bp::g_opt_gemm_wide.store(value); return BP_OK;
     default: bp::set_error("bp_set_option: unknown option %d", option); return BP_ERR_INVALID;
   }
 }

@@ -437,13 +437,20 @@ BP_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 // kernel (L2 -> SM bandwidth is the bound there).
 template <int BN_, bool B_MN_>
 struct Tc2Cfg {
+  // BN = pair-tile width; wider than 256 is issued as NSUB MMAs of N = 256
+  // per k-step into adjacent TMEM columns (one accumulator buffer then).
   static constexpr int BM = 128, BN = BN_, BNH = BN_ / 2, BK = 64;
-  static constexpr int BCH = (BNH + 63) / 64;  // 64-wide chunks of an MN-major B half
+  static constexpr int NSUB = BN_ > 256 ? BN_ / 256 : 1;
+  static constexpr int MMA_N = BN_ / NSUB;
+  static constexpr int SUBH = MMA_N / 2;        // B rows per CTA per sub-MMA
+  static constexpr int BCH = (SUBH + 63) / 64;  // 64-wide chunks of an MN-major B sub-half
   static constexpr uint32_t A_BYTES = BM * BK * 2;
-  static constexpr uint32_t B_BYTES = B_MN_ ? BCH * 64 * BK * 2 : BNH * BK * 2;
+  static constexpr uint32_t SUB_BYTES = B_MN_ ? BCH * 64 * BK * 2 : SUBH * BK * 2;
+  static constexpr uint32_t B_BYTES = NSUB * SUB_BYTES;
   static constexpr int STAGES = (200 * 1024) / (A_BYTES + B_BYTES) > 8 ? 8 : (200 * 1024) / (A_BYTES + B_BYTES);
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr uint32_t TMEM_COLS = 2 * BN <= 256 ? 256 : 512;  // power of two
+  static constexpr int ACC = 2 * BN_ <= 512 ? 2 : 1;  // TMEM accumulator buffers
+  static constexpr uint32_t TMEM_COLS = ACC * BN_ <= 256 ? 256 : 512;  // power of two
   static constexpr size_t SMEM = 1024 + STAGES * (size_t)STAGE_BYTES + 256;
 };
 
@@ -483,7 +490,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       mbar_init(&full[s], 2);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < C::ACC; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 256);
     }
@@ -503,7 +510,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         const Seg sg = sch.get(si);
         const int tile = sg.tile;
         const int m0 = (tile % tiles_m) * 256 + rank * 128;
-        const int n0 = (tile / tiles_m) * C::BN + rank * C::BNH;
+        const int n0 = (tile / tiles_m) * C::BN + rank * C::SUBH;
         for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * C::A_BYTES;
@@ -515,12 +522,17 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
 #pragma unroll
             for (int c = 0; c < 2; ++c) tma_load_2d_2sm(a + c * (BK * 128), &map_a, m0 + 64 * c, k0, &full[stage]);
           }
-          if (!B_MN) {
-            tma_load_2d_2sm(b, &map_b, k0, n0, &full[stage]);
-          } else {
 #pragma unroll
-            for (int c = 0; c < C::BCH; ++c)
-              tma_load_2d_2sm(b + c * (BK * 128), &map_b, n0 + 64 * c, k0, &full[stage]);
+          for (int j = 0; j < C::NSUB; ++j) {
+            const int nj = n0 + j * C::MMA_N;
+            uint8_t* bj = b + j * C::SUB_BYTES;
+            if (!B_MN) {
+              tma_load_2d_2sm(bj, &map_b, k0, nj, &full[stage]);
+            } else {
+#pragma unroll
+              for (int c = 0; c < C::BCH; ++c)
+                tma_load_2d_2sm(bj + c * (BK * 128), &map_b, nj + 64 * c, k0, &full[stage]);
+            }
           }
           if (leader)
             mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
@@ -532,14 +544,14 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only)
-      constexpr uint32_t idesc = umma_idesc_bf16(256, C::BN, A_MN, B_MN);
+      constexpr uint32_t idesc = umma_idesc_bf16(256, C::MMA_N, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
       for (int si = 0; si < nseg; ++si, ++it) {
         const Seg sg = sch.get(si);
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
+        const int acc = C::ACC == 2 ? (it & 1) : 0;
+        const uint32_t acc_phase = C::ACC == 2 ? ((it >> 1) & 1) : (it & 1);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * C::BN;
@@ -552,9 +564,13 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = A_MN ? umma_desc_sw128(a_addr + k * 2048, BK * 128, 1024)
                                      : umma_desc_sw128(a_addr + k * 32, 0, 1024);
-            const uint64_t bd = B_MN ? umma_desc_sw128(b_addr + k * 2048, BK * 128, 1024)
-                                     : umma_desc_sw128(b_addr + k * 32, 0, 1024);
-            tc_mma_f16_2sm(d_tmem, ad, bd, idesc, (kb > sg.kb0) || (k != 0));
+#pragma unroll
+            for (int j = 0; j < C::NSUB; ++j) {
+              const uint32_t bj = b_addr + j * C::SUB_BYTES;
+              const uint64_t bd = B_MN ? umma_desc_sw128(bj + k * 2048, BK * 128, 1024)
+                                       : umma_desc_sw128(bj + k * 32, 0, 1024);
+              tc_mma_f16_2sm(d_tmem + j * C::MMA_N, ad, bd, idesc, (kb > sg.kb0) || (k != 0));
+            }
           }
           tc_commit_2sm_mc(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -568,8 +584,8 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     for (int si = 0; si < nseg; ++si, ++it) {
       const Seg sg = sch.get(si);
       const int tile = sg.tile;
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      const int acc = C::ACC == 2 ? (it & 1) : 0;
+      const uint32_t acc_phase = C::ACC == 2 ? ((it >> 1) & 1) : (it & 1);
       const int m0 = (tile % tiles_m) * 256 + rank * 128;
       const int n0 = (tile / tiles_m) * C::BN;
       mbar_wait(&tfull[acc], acc_phase);
@@ -826,7 +842,7 @@ static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
     rc = make_map(&ma, g.A, g.M, g.K, g.lda, 64, 64);
   if (rc) return rc;
   if (!B_MN)
-    rc = make_map(&mb, g.B, g.K, g.N, g.ldb, 64, C::BNH);
+    rc = make_map(&mb, g.B, g.K, g.N, g.ldb, 64, C::SUBH);
   else
     rc = make_map(&mb, g.B, g.N, g.K, g.ldb, 64, 64);
   if (rc) return rc;
@@ -872,19 +888,26 @@ static int dispatch_tc2_bn(const bp_gemm_args& g, const Epi& ep, cudaStream_t st
 // Model the time of a launch as rounds(BN) * (128 + BN/2) -- the wave
 // quantisation over 74 CTA pairs times the per-tile operand traffic -- and
 // pick the minimum (N = 8192 at M = 2048: 224 gives exactly 4 waves).
+int gemm_wide_mode();
+
 int pick_tc2_bn(int M, int N, int pairs, bool b_mn_major) {
-  static const int cand[4] = {256, 224, 192, 128};
+  static const int cand[5] = {256, 512, 224, 192, 128};
   const int tm = (M + 255) / 256;
   int best = 256;
   long best_score = -1;
-  for (int i = 0; i < 4; ++i) {
+  const int wide = gemm_wide_mode();
+  for (int i = 0; i < 5; ++i) {
     const int bn = cand[i];
+    if (bn == 512 && wide != 1) continue;  // measured slower than 256 on every shape: opt-in only
+    if (wide == 1 && bn != 512 && N >= 512) continue;  // testing aid: force 512
     // an MN-major B half of 112 / 96 columns still loads two full 64-wide
     // TMA boxes; measured slower than 256, so only K-major B narrows
     if (b_mn_major && (bn == 224 || bn == 192)) continue;
     const long tiles = (long)tm * ((N + bn - 1) / bn);
     const long rounds = (tiles + pairs - 1) / pairs;
-    const long score = rounds * (128 + bn / 2);
+    // 512-wide tiles have a single TMEM accumulator: the epilogue is not
+    // hidden behind the next tile's MMAs (~12% of a K = 2048 tile)
+    const long score = rounds * (128 + bn / 2) * (bn == 512 ? 112 : 100) / 100;
     if (best_score < 0 || score < best_score) {
       best_score = score;
       best = bn;
@@ -895,6 +918,7 @@ int pick_tc2_bn(int M, int N, int pairs, bool b_mn_major) {
 
 static int dispatch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   switch (pick_tc2_bn(g.M, g.N, num_sms() / 2, !g.b_kmajor)) {
+    case 512: return dispatch_tc2_bn<512>(g, ep, st);
     case 224: return dispatch_tc2_bn<224>(g, ep, st);
     case 192: return dispatch_tc2_bn<192>(g, ep, st);
     case 128: return dispatch_tc2_bn<128>(g, ep, st);

@@ -286,8 +286,34 @@ def test_gemm_stream_k_matches_data_parallel(M, N, K, ak, bk, acc):
             torch.cuda.synchronize()
             outs.append(C2)
         finally:
-            ops.set_option(OPT_STREAM_K, 0)
+            ops.set_option(OPT_STREAM_K, 2)
     opA = A.float() if ak else A.float().t()
     opB = B.float().t() if bk else B.float()
     ref = opA @ opB + (base if acc else 0)
     assert _relerr(outs[0], ref) < 1e-5 and _relerr(outs[1], ref) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(2048, 8192, 2048), (512, 1024, 256), (300, 520, 192), (8192, 2048, 128),
+                                   (2048, 50304 // 8, 128)])
+@pytest.mark.parametrize("ak,bk", [(True, True), (True, False), (False, False), (False, True)])
+def test_gemm_wide_pair_tiles(M, N, K, ak, bk):
+    """256 x 512 pair tiles (two N=256 MMAs per k-step, one TMEM buffer)."""
+    from paper_2410_19367_b200.runtime.lib import OPT_GEMM_WIDE
+    ops.set_option(OPT_GEMM_WIDE, 1)
+    try:
+        A = (torch.randn(M, K) if ak else torch.randn(K, M)).cuda().bfloat16()
+        B = (torch.randn(N, K) if bk else torch.randn(K, N)).cuda().bfloat16()
+        bias = torch.randn(N, device="cuda").bfloat16()
+        C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        ops.gemm(A, B, C, a_kmajor=ak, b_kmajor=bk, bias=bias)
+        C32 = torch.randn(M, N, device="cuda")
+        base = C32.clone()
+        ops.gemm(A, B, C32, a_kmajor=ak, b_kmajor=bk, beta=1.0)
+        torch.cuda.synchronize()
+    finally:
+        ops.set_option(OPT_GEMM_WIDE, 0)
+    opA = A.float() if ak else A.float().t()
+    opB = B.float().t() if bk else B.float()
+    ref = opA @ opB
+    assert _relerr(C.float(), ref + bias.float()) < 1e-2
+    assert _relerr(C32, base + ref) < 1e-5
