@@ -33,6 +33,14 @@ int make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, 
 
 namespace fat {
 
+#ifdef BP_ATTN_TRACE
+__device__ long long g_trace[64][8];
+#define TRACE(it, k) \
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 128 && (it) < 64) g_trace[(it)][(k)] = clock64();
+#else
+#define TRACE(it, k)
+#endif
+
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -40,6 +48,18 @@ constexpr float kLn2 = 0.6931471805599453f;
 // tile whose K extent is split into 64-element atoms of `rows` x 128 B.
 BP_DEV uint32_t kmaj_off(int r, int u, int rows) {
   return (uint32_t)((u >> 3) * rows * 128 + r * 128 + (((u & 7) ^ (r & 7)) << 4));
+}
+
+// 2^x in one MUFU op (flush-to-zero; inputs here are <= ~8 or -inf).
+BP_DEV float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+BP_DEV float lds(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
 }
 
 BP_DEV uint4 pack8(const float* f) {
@@ -209,7 +229,7 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
           mbar_wait(pv_done, (j - 1) & 1);
           waited = true;
           tc_fence_after();
-          const float f = exp2f(m_used - mx);
+          const float f = ex2(m_used - mx);
 #pragma unroll 1
           for (int c = 0; c < Dh / 32; ++c) {
             float ov[32];
@@ -225,7 +245,7 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       float lsum = 0.f;
 #pragma unroll
       for (int i = 0; i < 128; ++i) {
-        s[i] = exp2f(s[i] - m_used);
+        s[i] = ex2(s[i] - m_used);
         lsum += s[i];
       }
       l += lsum;
@@ -391,26 +411,33 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
     const uint32_t aP = smem_u32(sP), aD = smem_u32(sD);
     for (int it = 0; it < n_it; ++it) {
       const int st = it & 1, qi = q0 + it;
+      TRACE(it, 0);
       mbar_wait(&q_full[st], (it >> 1) & 1);  // lse / delta of this tile are in smem
+      TRACE(it, 1);
       mbar_wait(sdp_full, it & 1);
+      TRACE(it, 2);
       tc_fence_after();
       float sv[64], dp[64];
       tmem_ld_32x32b_x32(tl + 0, *reinterpret_cast<float(*)[32]>(sv));
       tmem_ld_32x32b_x32(tl + 32, *reinterpret_cast<float(*)[32]>(sv + 32));
       tmem_ld_32x32b_x32(tl + 64, *reinterpret_cast<float(*)[32]>(dp));
       tmem_ld_32x32b_x32(tl + 96, *reinterpret_cast<float(*)[32]>(dp + 32));
+      TRACE(it, 3);
       tc_fence_before();
       mbar_arrive(sdp_free);
-      const float* L = sL[st];
+      const uint32_t aL = smem_u32(sL[st]);
+      const bool diag = CAUSAL && qi * 64 < key;  // some query of this tile precedes the key
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
         const int q = qi * 64 + i;
-        float p = exp2f(sv[i] * scale_log2 - L[i] * kLog2e);
-        if (CAUSAL && q < key) p = 0.f;
+        float p = ex2(fmaf(sv[i], scale_log2, -lds(aL + 4 * i) * kLog2e));
+        if (diag && q < key) p = 0.f;
         sv[i] = p;
-        dp[i] = p * (dp[i] - L[64 + i]);
+        dp[i] = p * (dp[i] - lds(aL + 256 + 4 * i));
       }
+      TRACE(it, 4);
       if (it > 0) mbar_wait(mm_done, (it - 1) & 1);
+      TRACE(it, 5);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         st_shared_v4(aP + kmaj_off(r, u, 128), pack8(sv + 8 * u));
@@ -419,6 +446,7 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(p_full);
+      TRACE(it, 6);
     }
     // epilogue: dV, dK (scaled) -> dqkv
     if (n_it > 0) mbar_wait(mm_done, (n_it - 1) & 1);
@@ -585,7 +613,7 @@ dq_tc(const __grid_constant__ CUtensorMap map_q128, const __grid_constant__ CUte
       const bool diag = CAUSAL && (it * 64 + 63 > q);
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
-        float p = exp2f(sv[i] * scale_log2 - lse2);
+        float p = ex2(fmaf(sv[i], scale_log2, -lse2));
         if (diag && it * 64 + i > q) p = 0.f;
         dp[i] = p * (dp[i] - dl);
       }
@@ -690,6 +718,16 @@ static int bwd(int B, int S, int H, float scale, const void* qkv, const void* o,
 }
 
 }  // namespace fat
+
+// Debug aid (BP_ATTN_TRACE builds): copy the dK/dV softmax-warp timestamps.
+extern "C" int bp_attn_trace_dump(long long* host, int n) {
+#ifdef BP_ATTN_TRACE
+  return cudaMemcpyFromSymbol(host, fat::g_trace, sizeof(long long) * (n < 512 ? n : 512)) == cudaSuccess ? 0 : 2;
+#else
+  (void)host; (void)n;
+  return 3;
+#endif
+}
 
 bool attn_tc_supported(int dtype, int S, int Dh) {
   return dtype == BP_BF16 && (Dh == 64 || Dh == 128) && S >= 128 && S % 128 == 0 && !opt_attn_no_tc();

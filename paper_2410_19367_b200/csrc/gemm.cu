@@ -127,14 +127,20 @@ BP_DEV void epi_row32(const Epi& ep, int r, int c0, float (&v)[32]) {
     store32(ep.aux, ep.c_dtype, ao, v);
     if (ep.c_dtype == BP_BF16) {  // gelu of the rounded pre-activation
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
-    }
+      for (int i = 0; i < 32; ++i) v[i] = gelu_fast(__bfloat162float(__float2bfloat16_rn(v[i])));
+    } else {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i]);
+      for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i]);
+    }
   } else if (ep.epilogue == BP_EPI_DGELU) {
     load32(ep.aux, ep.c_dtype, (int64_t)r * ep.ldaux + c0, t);
+    if (ep.c_dtype == BP_BF16) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(t[i]);
+      for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_fast(t[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(t[i]);
+    }
   }
   if (ep.residual) {
     load32(ep.residual, ep.c_dtype, (int64_t)r * ep.ldr + c0, t);
@@ -201,8 +207,13 @@ BP_DEV void epi_tile(const Epi& ep, uint32_t tmem_addr, int row, int n0) {
       for (int i = 0; i < 32; ++i) v[i] += t[i];
     }
     if (ep.epilogue == BP_EPI_DGELU) {
+      if (ep.c_dtype == BP_BF16) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(cur[i]);
+        for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_fast(cur[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(cur[i]);
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] += cur[i];
