@@ -67,8 +67,11 @@ enum bp_option {
   BP_OPT_STREAM_K = 4,   /* stream-K GEMM scheduling: 0 auto (sub-wave, K >= 4096
                             only), 1 every ragged last wave, 2 off (default:
                             measured slower on the GPT-1.3B shapes)          */
-  BP_OPT_GEMM_WIDE = 5   /* 256 x 512 pair tiles: 1 force (default 0: never,
+  BP_OPT_GEMM_WIDE = 5,  /* 256 x 512 pair tiles: 1 force (default 0: never,
                             measured slower than 256 x 256)                  */
+  BP_OPT_GEMM_DEBUG = 6,  /* 1: skip the GEMM epilogue stores (profiling only) */
+  BP_OPT_GEMM_TMA_STORE = 7  /* 1 (default): 2-SM GEMM epilogue writes through
+                                smem + TMA bulk stores; 0: per-thread stores */
 };
 BP_API int bp_set_option(int option, int value);
 

@@ -12,7 +12,7 @@ namespace bp {
 
 static thread_local char g_err[1024] = "";
 static std::atomic<unsigned long long> g_launches{0};
-static std::atomic<int> g_opt_attn_exact{0}, g_opt_gemm_simt{0}, g_opt_gemm_mode{0}, g_opt_stream_k{2}, g_opt_gemm_wide{0};
+static std::atomic<int> g_opt_attn_exact{0}, g_opt_gemm_simt{0}, g_opt_gemm_mode{0}, g_opt_stream_k{2}, g_opt_gemm_wide{0}, g_opt_gemm_debug{0}, g_opt_gemm_tma_store{1};
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -46,6 +46,8 @@ bool opt_gemm_simt() { return g_opt_gemm_simt.load() != 0; }
 int gemm_mode() { return g_opt_gemm_mode.load(); }
 int stream_k_mode() { return g_opt_stream_k.load(); }
 int gemm_wide_mode() { return g_opt_gemm_wide.load(); }
+int gemm_debug_nostore() { return g_opt_gemm_debug.load() == 1; }
+int gemm_tma_store_mode() { return g_opt_gemm_tma_store.load(); }
 
 }  // namespace bp
 
@@ -79,6 +81,8 @@ int bp_set_option(int option, int value) {
     case BP_OPT_GEMM_MODE: bp::g_opt_gemm_mode.store(value); return BP_OK;
     case BP_OPT_STREAM_K: bp::g_opt_stream_k.store(value); return BP_OK;
     case BP_OPT_GEMM_WIDE: bp::g_opt_gemm_wide.store(value); return BP_OK;
+    case BP_OPT_GEMM_DEBUG: bp::g_opt_gemm_debug.store(value); return BP_OK;
+    case BP_OPT_GEMM_TMA_STORE: bp::g_opt_gemm_tma_store.store(value); return BP_OK;
     default: bp::set_error("bp_set_option: unknown option %d", option); return BP_ERR_INVALID;
   }
 }

@@ -36,6 +36,8 @@ struct Epi {
   int64_t ldaux;
   int epilogue;
   int vec_ok;
+  int nostore;  // debug: drain TMEM but skip the global epilogue (BP_OPT_GEMM_DEBUG)
+  int tma_store;  // 2-SM kernel: stage 32-column chunks in smem, TMA-store them
 };
 
 BP_DEV float ld_any(const void* p, int dtype, int64_t i) {
@@ -109,7 +111,7 @@ BP_DEV void store32(void* p, int dtype, int64_t off, const float (&x)[32]) {
 }
 
 BP_DEV void epi_row32(const Epi& ep, int r, int c0, float (&v)[32]) {
-  if (r >= ep.M) return;
+  if (r >= ep.M || ep.nostore) return;
   if (!ep.vec_ok || c0 + 32 > ep.N) {
     for (int i = 0; i < 32 && c0 + i < ep.N; ++i) epi_one(ep, r, c0 + i, v[i]);
     return;
@@ -163,6 +165,15 @@ BP_DEV void epi_row32(const Epi& ep, int r, int c0, float (&v)[32]) {
 // latency of the read-modify-write is not serialised across chunks.
 template <int NCHUNK>
 BP_DEV void epi_tile(const Epi& ep, uint32_t tmem_addr, int row, int n0) {
+  if (ep.nostore) {
+#pragma unroll 1
+    for (int c = 0; c < NCHUNK; ++c) {
+      float v[32];
+      tmem_ld_32x32b_x32(tmem_addr + c * 32, v);
+      if (v[0] == 12345.f) static_cast<float*>(ep.C)[0] = v[1];  // keep the load live
+    }
+    return;
+  }
   const void* xin = nullptr;
   int xdt = ep.c_dtype;
   int64_t xld = 0;
@@ -219,6 +230,133 @@ BP_DEV void epi_tile(const Epi& ep, uint32_t tmem_addr, int row, int n0) {
       for (int i = 0; i < 32; ++i) v[i] += cur[i];
     }
     store32(ep.C, ep.c_dtype, (int64_t)row * ep.ldc + c0, v);
+  }
+}
+
+// TMA-store epilogue of one accumulator slice (warp = 32 TMEM lanes = 32
+// rows, NCHUNK x 32 columns).  Each 32-column chunk is finished in
+// registers, written to a per-warp shared staging unit in the TMA swizzle
+// (bf16: 64-byte rows, SWIZZLE_64B; fp32: 128-byte rows, SWIZZLE_128B --
+// conflict-free 16-byte stores), and sent with one bulk tensor store (a
+// bulk reduce-add for fp32 accumulation: C += tile happens at L2, C is
+// never read into the SM).  Replaces 32 rows x 16-byte scattered stores
+// per warp instruction with full-line bulk writes.  Two staging units per
+// warp alternate; `ubuf` carries the unit parity across tiles.  Rows past
+// M / columns past N are clipped by the TMA unit.
+BP_DEV void stage_row32(uint8_t* unit, int lane, int dtype, const float (&v)[32]) {
+  if (dtype == BP_F32) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t off = lane * 128 + ((j ^ (lane & 7)) << 4);
+      *reinterpret_cast<float4*>(unit + off) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint4 t;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&t);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) h[q] = __floats2bfloat162_rn(v[8 * j + 2 * q], v[8 * j + 2 * q + 1]);
+      const uint32_t off = lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
+      *reinterpret_cast<uint4*>(unit + off) = t;
+    }
+  }
+}
+
+// bf16 row of a SWIZZLE_64B staging unit -> 32 floats
+BP_DEV void unstage_row32_bf16(const uint8_t* unit, int lane, float (&x)[32]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint4 t = *reinterpret_cast<const uint4*>(unit + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&t);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = __bfloat1622float2(h[q]);
+      x[8 * j + 2 * q] = f.x;
+      x[8 * j + 2 * q + 1] = f.y;
+    }
+  }
+}
+
+// Per-warp state of the TMA epilogue, carried across tiles.
+struct EpiTma {
+  uint8_t* stage;    // 2 units x 4 KB: [0, 2K) output / [2K, 4K) aux-out or input
+  uint64_t* bar;     // 2 mbarriers (input tile landed in unit u)
+  int ubuf;          // next unit
+  uint32_t phase;    // bit u = parity of bar[u]
+};
+
+// The extra epilogue input (residual, or the saved pre-activation for
+// dGELU) arrives by TMA too: chunk c+1's 32 x 32 tile is requested while
+// chunk c is finished, into the upper half of the other unit.
+BP_DEV void epi_tma_prefetch_input(const CUtensorMap* mx, EpiTma& es, int u, int c0, int row0) {
+  uint8_t* dst = es.stage + u * 4096 + 2048;
+  fence_proxy_async_smem();  // earlier generic reads of this half precede the async write
+  mbar_expect_tx(&es.bar[u], 2048);
+  tma_load_2d(dst, mx, c0, row0, &es.bar[u]);
+}
+
+template <int NCHUNK>
+BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap* mx, uint32_t tmem_addr,
+                         int row0, int lane, int n0, EpiTma& es, bool input_issued) {
+  const bool gelu = ep.epilogue == BP_EPI_GELU;
+  const bool has_in = ep.residual != nullptr || ep.epilogue == BP_EPI_DGELU;
+  if (has_in && !input_issued && lane == 0) epi_tma_prefetch_input(mx, es, es.ubuf, n0, row0);
+#pragma unroll 1
+  for (int c = 0; c < NCHUNK; ++c) {
+    const int c0 = n0 + c * 32;
+    if (c0 >= ep.N) break;  // warp-uniform
+    const int u = es.ubuf;
+    uint8_t* unit = es.stage + u * 4096;
+    if (has_in && lane == 0 && c + 1 < NCHUNK && c0 + 32 < ep.N)
+      epi_tma_prefetch_input(mx, es, u ^ 1, c0 + 32, row0);
+    float v[32];
+    tmem_ld_32x32b_x32(tmem_addr + c * 32, v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= ep.alpha;
+    if (ep.bias) {
+      float t[32];
+      load32(ep.bias, ep.bias_dtype, c0, t);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += t[i];
+    }
+    if (has_in) {
+      float cur[32];
+      mbar_wait(&es.bar[u], (es.phase >> u) & 1);
+      es.phase ^= 1u << u;
+      unstage_row32_bf16(unit + 2048, lane, cur);
+      if (ep.epilogue == BP_EPI_DGELU) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_fast(cur[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] += cur[i];
+      }
+    }
+    if (lane == 0) bulk_wait_read<1>();  // this unit's previous store has read it
+    __syncwarp();
+    if (gelu) {
+      stage_row32(unit + 2048, lane, ep.c_dtype, v);  // pre-activation -> aux
+      if (ep.c_dtype == BP_BF16) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = gelu_fast(__bfloat162float(__float2bfloat16_rn(v[i])));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i]);
+      }
+    }
+    stage_row32(unit, lane, ep.c_dtype, v);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      if (ep.accumulate)
+        tma_reduce_add_2d(mc, unit, c0, row0);
+      else
+        tma_store_2d(mc, unit, c0, row0);
+      if (gelu) tma_store_2d(mx, unit + 2048, c0, row0);
+      bulk_commit();
+    }
+    es.ubuf ^= 1;
   }
 }
 
@@ -458,16 +596,19 @@ struct Tc2Cfg {
   static constexpr uint32_t A_BYTES = BM * BK * 2;
   static constexpr uint32_t SUB_BYTES = B_MN_ ? BCH * 64 * BK * 2 : SUBH * BK * 2;
   static constexpr uint32_t B_BYTES = NSUB * SUB_BYTES;
-  static constexpr int STAGES = (200 * 1024) / (A_BYTES + B_BYTES) > 8 ? 8 : (200 * 1024) / (A_BYTES + B_BYTES);
+  static constexpr uint32_t EPI_BYTES = 4 * 2 * 4096;  // 2 TMA-store staging units per epilogue warp
+  static constexpr int STAGE_BUDGET = 232448 - 1024 - 256 - (int)EPI_BYTES;
+  static constexpr int STAGES = STAGE_BUDGET / (A_BYTES + B_BYTES) > 8 ? 8 : STAGE_BUDGET / (A_BYTES + B_BYTES);
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int ACC = 2 * BN_ <= 512 ? 2 : 1;  // TMEM accumulator buffers
   static constexpr uint32_t TMEM_COLS = ACC * BN_ <= 256 ? 256 : 512;  // power of two
-  static constexpr size_t SMEM = 1024 + STAGES * (size_t)STAGE_BYTES + 256;
+  static constexpr size_t SMEM = 1024 + STAGES * (size_t)STAGE_BYTES + EPI_BYTES + 256;
 };
 
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_aux,
                 int M, int N, int K, Epi ep, SkWs ws) {
   using C = Tc2Cfg<BN, B_MN>;
   constexpr int BK = C::BK, STAGES = C::STAGES;
@@ -475,11 +616,13 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+  uint8_t* sEpi = sB + STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + C::EPI_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ebar = tempty + 2;  // 4 epilogue warps x 2 input-tile barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -505,6 +648,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 256);
     }
+    for (int e = 0; e < 8; ++e) mbar_init(&ebar[e], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_2sm<C::TMEM_COLS>(tmem_slot);
@@ -592,6 +736,12 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   } else if (warp >= 4) {  // ---------------------- epilogue (both CTAs)
     const int ew = warp - 4;
     int it = 0;
+    EpiTma es{sEpi + ew * 8192, ebar + 2 * ew, 0, 0u};
+    const bool tma_in = ep.tma_store && (ep.residual != nullptr || ep.epilogue == BP_EPI_DGELU);
+    if (ep.tma_store && lane == 0) {
+      tma_prefetch_desc(&map_c);
+      if (ep.epilogue != BP_EPI_NONE || ep.residual) tma_prefetch_desc(&map_aux);
+    }
     for (int si = 0; si < nseg; ++si, ++it) {
       const Seg sg = sch.get(si);
       const int tile = sg.tile;
@@ -599,6 +749,8 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       const uint32_t acc_phase = C::ACC == 2 ? ((it >> 1) & 1) : (it & 1);
       const int m0 = (tile % tiles_m) * 256 + rank * 128;
       const int n0 = (tile / tiles_m) * C::BN;
+      // the first input tile is requested before waiting for the accumulator
+      if (tma_in && sg.role == 0 && lane == 0) epi_tma_prefetch_input(&map_aux, es, es.ubuf, n0, m0 + ew * 32);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = m0 + ew * 32 + lane;
@@ -651,6 +803,8 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           for (int i = 0; i < 32; ++i) v[i] += cur[i];
           if (n0 + c * 32 < N) epi_row32(ep, row, n0 + c * 32, v);
         }
+      } else if (ep.tma_store) {
+        epi_tile_tma<C::BN / 32>(ep, &map_c, &map_aux, t0, m0 + ew * 32, lane, n0, es, tma_in);
       } else {
         epi_tile<C::BN / 32>(ep, t0, row, n0);
       }
@@ -660,6 +814,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       else
         mbar_arrive_remote(&tempty[acc], 0);
     }
+    if (ep.tma_store && lane == 0) bulk_wait<0>();  // stores complete before the CTA retires
   }
   __syncthreads();
   cluster_sync();
@@ -737,26 +892,33 @@ static EncodeTiledFn encode_fn() {
 
 // bf16 2-D map over a row-major matrix with `inner` contiguous elements per
 // row (row pitch `ld` elements) and `outer` rows; box = box_inner x box_outer.
-int make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, int64_t ld,
-             uint32_t box_inner, uint32_t box_outer) {
+int make_map_dt(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, int64_t ld,
+                uint32_t box_inner, uint32_t box_outer, int dtype, int swizzle_bytes) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return BP_ERR_CUDA;
   }
+  const int esz = dtype == BP_F32 ? 4 : 2;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * esz};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUtensorMapSwizzle sw = swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+  CUresult r = enc(map, dtype == BP_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu ld=%lld box=%ux%u", (int)r,
               (unsigned long long)inner, (unsigned long long)outer, (long long)ld, box_inner, box_outer);
     return BP_ERR_INVALID;
   }
   return BP_OK;
+}
+
+int make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, int64_t ld, uint32_t box_inner,
+             uint32_t box_outer) {
+  return make_map_dt(map, ptr, inner, outer, ld, box_inner, box_outer, BP_BF16, 128);
 }
 
 void count_launch();
@@ -817,6 +979,8 @@ static std::mutex g_sk_mu;
 static std::unordered_map<uint64_t, SkWsState> g_sk;
 
 int stream_k_mode();
+int gemm_debug_nostore();
+int gemm_tma_store_mode();
 
 static int sk_workspace(cudaStream_t st, size_t floats, int nflag, SkWs* out) {
   int dev = 0;
@@ -857,6 +1021,20 @@ static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   else
     rc = make_map(&mb, g.B, g.N, g.K, g.ldb, 64, 64);
   if (rc) return rc;
+  // epilogue staging unit = 32 rows x 32 columns (bf16: 64 B rows, fp32: 128 B rows)
+  CUtensorMap mc, maux;
+  memset(&mc, 0, sizeof(mc));
+  memset(&maux, 0, sizeof(maux));
+  if (ep.tma_store) {
+    const int sw = g.c_dtype == BP_F32 ? 128 : 64;
+    if ((rc = make_map_dt(&mc, g.C, g.N, g.M, g.ldc, 32, 32, g.c_dtype, sw))) return rc;
+    // aux map: GELU pre-activation output, dGELU input, or the residual input
+    if (g.epilogue != BP_EPI_NONE) {
+      if ((rc = make_map_dt(&maux, g.aux, g.N, g.M, g.ldaux, 32, 32, g.c_dtype, sw))) return rc;
+    } else if (g.residual) {
+      if ((rc = make_map_dt(&maux, g.residual, g.N, g.M, g.ldr, 32, 32, g.c_dtype, sw))) return rc;
+    }
+  }
   auto kern = gemm_tc2_kernel<BN, A_MN, B_MN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -878,7 +1056,7 @@ static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   if (ws.enable) {
     if (int rc = sk_workspace(st, (size_t)npairs * 2 * 128 * C::BN, npairs * 2, &ws)) return rc;
   }
-  kern<<<2 * npairs, 256, C::SMEM, st>>>(ma, mb, g.M, g.N, g.K, ep, ws);
+  kern<<<2 * npairs, 256, C::SMEM, st>>>(ma, mb, mc, maux, g.M, g.N, g.K, ep, ws);
   count_launch();
   BP_CHECK_LAUNCH("gemm_tc2");
   return BP_OK;
@@ -966,6 +1144,8 @@ extern "C" int bp_gemm(const bp_gemm_args* gp, void* stream) {
   ep.M = g.M; ep.N = g.N; ep.C = g.C; ep.ldc = g.ldc; ep.c_dtype = g.c_dtype; ep.alpha = g.alpha;
   ep.accumulate = g.beta != 0.f; ep.bias = g.bias; ep.bias_dtype = g.in_dtype;
   ep.residual = g.residual; ep.ldr = g.ldr; ep.aux = g.aux; ep.ldaux = g.ldaux; ep.epilogue = g.epilogue;
+  ep.nostore = gemm_debug_nostore();
+  ep.tma_store = 0;
   const int esz = g.c_dtype == BP_F32 ? 4 : 2;
   ep.vec_ok = aligned16(g.C) && (g.ldc * esz) % 16 == 0 && (!g.bias || aligned16(g.bias)) &&
               (!g.residual || (aligned16(g.residual) && (g.ldr * esz) % 16 == 0)) &&
@@ -975,7 +1155,17 @@ extern "C" int bp_gemm(const bp_gemm_args* gp, void* stream) {
   const bool tma_ok = aligned16(g.A) && aligned16(g.B) && (g.lda % 8) == 0 && (g.ldb % 8) == 0;
   if (g.in_dtype == BP_BF16 && !g.force_simt && !opt_gemm_simt() && tma_ok) {
     const int mode = gemm_mode();
-    if (mode == 2 || (mode == 0 && g.M >= 256 && g.N >= 256)) return dispatch_tc2(g, ep, st);
+    if (mode == 2 || (mode == 0 && g.M >= 256 && g.N >= 256)) {
+      // TMA-store epilogue: whole 32-column chunks, 16-byte aligned
+      // pitches, at most one extra epilogue input besides bias.
+      ep.tma_store = gemm_tma_store_mode() && ep.vec_ok && g.N % 32 == 0 &&
+                     (!ep.accumulate || g.c_dtype == BP_F32) &&
+                     // TMA-loaded inputs are staged as bf16
+                     ((!g.residual && g.epilogue != BP_EPI_DGELU) || g.c_dtype == BP_BF16) &&
+                     !(g.residual && (ep.accumulate || g.epilogue != BP_EPI_NONE)) &&
+                     !(ep.accumulate && g.epilogue != BP_EPI_NONE);
+      return dispatch_tc2(g, ep, st);
+    }
     const int tiles256 = ((g.M + 127) / 128) * ((g.N + 255) / 256);
     if (g.N > 128 && tiles256 >= num_sms()) return dispatch_tc<256>(g, ep, st);
     return dispatch_tc<128>(g, ep, st);

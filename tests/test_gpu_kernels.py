@@ -87,6 +87,48 @@ def test_gemm_epilogues(M, N, K, gemm_mode):
     torch.cuda.synchronize()
 
 
+@pytest.mark.parametrize("M,N,K,ak,bk", [(512, 768, 256, True, True), (300, 416, 128, True, True),
+                                          (768, 544, 192, False, False), (256, 1024, 64, True, False)])
+def test_gemm_tma_store_epilogue_bitwise(M, N, K, ak, bk):
+    """The TMA-store epilogue (staged in smem, bulk store / bulk reduce-add)
+    must give bit-identical results to the per-thread store epilogue for
+    every epilogue kind, including ragged M (300) and a ragged last N tile."""
+    from paper_2410_19367_b200.runtime.lib import OPT_GEMM_TMA_STORE
+    dev = "cuda"
+    X = (torch.randn(M, K, device=dev) if ak else torch.randn(K, M, device=dev)).bfloat16()
+    W = (torch.randn(N, K, device=dev) if bk else torch.randn(K, N, device=dev)).bfloat16()
+    b = torch.randn(N, device=dev).bfloat16()
+    R = torch.randn(M, N, device=dev).bfloat16()
+    A0 = torch.randn(M, N, device=dev).bfloat16()
+    C0 = torch.randn(M, N, device=dev)
+    outs = []
+    try:
+        for mode in (0, 1):
+            ops.set_option(OPT_GEMM_TMA_STORE, mode)
+            kw = dict(a_kmajor=ak, b_kmajor=bk)
+            plain = torch.full((M, N), 7.0, device=dev, dtype=torch.bfloat16)
+            ops.gemm(X, W, plain, bias=b, **kw)
+            res = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+            ops.gemm(X, W, res, bias=b, residual=R, **kw)
+            aux = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+            gel = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+            ops.gemm(X, W, gel, bias=b, aux=aux, epilogue=EPI_GELU, **kw)
+            dg = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+            ops.gemm(X, W, dg, aux=A0, epilogue=EPI_DGELU, **kw)
+            accum = C0.clone()
+            ops.gemm(X, W, accum, beta=1.0, alpha=0.5, **kw)
+            f32 = torch.empty(M, N, device=dev)
+            ops.gemm(X, W, f32, **kw)
+            torch.cuda.synchronize()
+            outs.append((plain, res, aux, gel, dg, accum, f32))
+    finally:
+        ops.set_option(OPT_GEMM_TMA_STORE, 1)
+    names = ("plain", "residual", "gelu-aux", "gelu", "dgelu", "accumulate", "fp32")
+    for n, a, t in zip(names, outs[0], outs[1]):
+        assert torch.equal(a.view(torch.int16) if a.dtype == torch.bfloat16 else a.view(torch.int32),
+                           t.view(torch.int16) if t.dtype == torch.bfloat16 else t.view(torch.int32)), n
+
+
 @pytest.mark.parametrize("ak,bk", [(True, True), (True, False), (False, False)])
 def test_gemm_fp32_simt_exact(ak, bk):
     M, N, K = 97, 65, 33
