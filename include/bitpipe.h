@@ -70,8 +70,11 @@ enum bp_option {
   BP_OPT_GEMM_WIDE = 5,  /* 256 x 512 pair tiles: 1 force (default 0: never,
                             measured slower than 256 x 256)                  */
   BP_OPT_GEMM_DEBUG = 6,  /* 1: skip the GEMM epilogue stores (profiling only) */
-  BP_OPT_GEMM_TMA_STORE = 7  /* 1 (default): 2-SM GEMM epilogue writes through
+  BP_OPT_GEMM_TMA_STORE = 7, /* 1 (default): 2-SM GEMM epilogue writes through
                                 smem + TMA bulk stores; 0: per-thread stores */
+  BP_OPT_LN_UNFUSED = 8,     /* 1: LayerNorm bwd as dx kernel + column kernels
+                                (default 0: one fused launch)                */
+  BP_OPT_LN_CTAS_PER_SM = 9  /* fused LayerNorm bwd: row blocks per SM (1..8) */
 };
 BP_API int bp_set_option(int option, int value);
 
@@ -115,6 +118,13 @@ BP_API int bp_layernorm_fwd(int dtype, int rows, int cols, const void* x, const 
 BP_API int bp_layernorm_bwd(int dtype, int rows, int cols, const void* dy, const void* x,
                      const void* gamma, const float* mean, const float* rstd,
                      const void* dres, void* dx, float* dgamma, float* dbeta, void* stream);
+/* as bp_layernorm_bwd, and dx_colsum[c] += sum_r dx[r, c] (the values as
+ * stored) when dx_colsum is non-NULL: the bias gradient of the preceding
+ * half-block's output projection, fused into the same launch.           */
+BP_API int bp_layernorm_bwd_ex(int dtype, int rows, int cols, const void* dy, const void* x,
+                     const void* gamma, const float* mean, const float* rstd,
+                     const void* dres, void* dx, float* dgamma, float* dbeta,
+                     float* dx_colsum, void* stream);
 
 /* ------------------------------------------------------- elementwise --- */
 /* out[r, :] += sum over rows of x (fp32 accumulate into out[cols]). */

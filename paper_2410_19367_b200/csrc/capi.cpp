@@ -12,7 +12,7 @@ namespace bp {
 
 static thread_local char g_err[1024] = "";
 static std::atomic<unsigned long long> g_launches{0};
-static std::atomic<int> g_opt_attn_exact{0}, g_opt_gemm_simt{0}, g_opt_gemm_mode{0}, g_opt_stream_k{2}, g_opt_gemm_wide{0}, g_opt_gemm_debug{0}, g_opt_gemm_tma_store{1};
+static std::atomic<int> g_opt_attn_exact{0}, g_opt_gemm_simt{0}, g_opt_gemm_mode{0}, g_opt_stream_k{2}, g_opt_gemm_wide{0}, g_opt_gemm_debug{0}, g_opt_gemm_tma_store{1}, g_opt_ln_unfused{0}, g_opt_ln_cps{1};
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -48,6 +48,8 @@ int stream_k_mode() { return g_opt_stream_k.load(); }
 int gemm_wide_mode() { return g_opt_gemm_wide.load(); }
 int gemm_debug_nostore() { return g_opt_gemm_debug.load() == 1; }
 int gemm_tma_store_mode() { return g_opt_gemm_tma_store.load(); }
+bool ln_bwd_unfused() { return g_opt_ln_unfused.load() != 0; }
+int ln_ctas_per_sm() { return g_opt_ln_cps.load(); }
 
 }  // namespace bp
 
@@ -83,6 +85,11 @@ int bp_set_option(int option, int value) {
     case BP_OPT_GEMM_WIDE: bp::g_opt_gemm_wide.store(value); return BP_OK;
     case BP_OPT_GEMM_DEBUG: bp::g_opt_gemm_debug.store(value); return BP_OK;
     case BP_OPT_GEMM_TMA_STORE: bp::g_opt_gemm_tma_store.store(value); return BP_OK;
+    case BP_OPT_LN_UNFUSED: bp::g_opt_ln_unfused.store(value); return BP_OK;
+    case BP_OPT_LN_CTAS_PER_SM:
+      if (value < 1 || value > 8) return BP_ERR_INVALID;
+      bp::g_opt_ln_cps.store(value);
+      return BP_OK;
     default: bp::set_error("bp_set_option: unknown option %d", option); return BP_ERR_INVALID;
   }
 }

@@ -130,6 +130,19 @@ BP_DEV uint32_t cluster_ctarank() {
 BP_DEV void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// 16-byte load from the shared memory of CTA `cta` of the cluster, at the
+// offset of `local` in this CTA (distributed shared memory)
+BP_DEV float4 dsmem_ld_v4(const float* local, uint32_t cta) {
+  float4 v;
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %4, %5;\n\t"
+      "ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [ra];\n}"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "r"(smem_u32(local)), "r"(cta)
+      : "memory");
+  return v;
+}
 // arrive on the mbarrier at the same smem offset in CTA `cta` of the cluster
 BP_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
   asm volatile(
@@ -218,6 +231,12 @@ BP_DEV void tmem_st_32x32b_x32(uint32_t taddr, const float (&v)[32]) {
 // Make generic-proxy shared-memory writes visible to the async proxy
 // (tensor core / TMA) before signalling the consumer.
 BP_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// 16-byte vector fp32 reduction into global memory (one L2 atomic op for
+// four consecutive floats; `p` 16-byte aligned).
+BP_DEV void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
 
 // 2-D TMA tile store shared -> global (bulk-group completion); elements
 // outside the tensor map's extent are clipped by the hardware.

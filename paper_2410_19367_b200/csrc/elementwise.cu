@@ -106,6 +106,10 @@ int launch_colred(int rows, int cols, const void* a, int64_t lda, const void* x,
 }
 template int launch_colred<float, 1>(int, int, const void*, int64_t, const void*, const float*, const float*,
                                      float*, float*, cudaStream_t);
+template int launch_colred<float, 0>(int, int, const void*, int64_t, const void*, const float*, const float*,
+                                     float*, float*, cudaStream_t);
+template int launch_colred<__nv_bfloat16, 0>(int, int, const void*, int64_t, const void*, const float*,
+                                             const float*, float*, float*, cudaStream_t);
 template int launch_colred<__nv_bfloat16, 1>(int, int, const void*, int64_t, const void*, const float*,
                                              const float*, float*, float*, cudaStream_t);
 

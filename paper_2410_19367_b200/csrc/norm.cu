@@ -11,6 +11,8 @@
 namespace bp {
 void count_launch();
 int num_sms();
+bool ln_bwd_unfused();
+int ln_ctas_per_sm();
 template <typename T, int MODE>
 int launch_colred(int rows, int cols, const void* a, int64_t lda, const void* x, const float* mean, const float* rstd,
                   float* out0, float* out1, cudaStream_t st);
@@ -158,6 +160,155 @@ __global__ void __launch_bounds__(256) ln_bwd_warp(int rows, const T* __restrict
   }
 }
 
+// Fused backward: dx, dgamma, dbeta and (optionally) the column sum of dx
+// in one launch.  A CTA owns a contiguous run of rows and all columns.
+// Phase 1 (warp per row): the two row reductions (mean of dy*g and of
+// dy*g*xhat) into shared memory.  Phase 2 (thread per 16-byte column
+// vector): walk the rows, write dx and accumulate the column sums in
+// registers; one fp32 atomicAdd per column and output at the end.  The
+// phase-2 re-read of dy / x hits L2 (the CTA's rows were just read).
+// The column sum of dx is the bias gradient of the preceding half-block's
+// output projection (its output gradient IS this dx), taken over the
+// values as stored.
+// RG row groups of 32*NV threads: phase 2 runs RG rows at a time, so a
+// CTA of rows finishes in ~2 memory round trips instead of rows_per.
+template <typename T, int NV, int RG>
+__global__ void __launch_bounds__(32 * NV * RG) ln_bwd_fused(int rows, int rows_per, const T* __restrict__ dy,
+                                                             const T* __restrict__ x, const T* __restrict__ g,
+                                                             const float* __restrict__ mean,
+                                                             const float* __restrict__ rstd,
+                                                             const T* __restrict__ dres, T* __restrict__ dx,
+                                                             float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                                             float* __restrict__ dxsum) {
+  using V = Vec<T>;
+  using U = typename V::U;
+  constexpr int E = V::N;
+  constexpr int nvec = 32 * NV;  // 16-byte vectors per row
+  constexpr int cols = nvec * E;
+  constexpr int NW = NV * RG;    // warps per CTA
+  extern __shared__ float sstat[];  // [rows_per][4]: s1, s2, mu, rs; then [RG-1][3][cols] partials
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = blockIdx.x * rows_per, r1 = min(rows, r0 + rows_per);
+  const U* DY = reinterpret_cast<const U*>(dy);
+  const U* X = reinterpret_cast<const U*>(x);
+  const U* G = reinterpret_cast<const U*>(g);
+  for (int r = r0 + warp; r < r1; r += NW) {
+    const float mu = mean[r], rs = rstd[r];
+    constexpr int CH = NV < 8 ? NV : 8;  // vectors in flight per lane
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i0 = 0; i0 < NV; i0 += CH) {
+      U pa[CH], pd[CH], pg[CH];
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        pa[i] = X[(int64_t)r * nvec + (i0 + i) * 32 + lane];
+        pd[i] = DY[(int64_t)r * nvec + (i0 + i) * 32 + lane];
+        pg[i] = G[(i0 + i) * 32 + lane];
+      }
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        float a[E], d[E], gg[E];
+        V::unpack(pa[i], a);
+        V::unpack(pd[i], d);
+        V::unpack(pg[i], gg);
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          const float dh = d[j] * gg[j];
+          s1 += dh;
+          s2 += dh * (a[j] - mu) * rs;
+        }
+      }
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+      float* q = sstat + 4 * (r - r0);
+      q[0] = s1 * (1.f / cols);
+      q[1] = s2 * (1.f / cols);
+      q[2] = mu;
+      q[3] = rs;
+    }
+  }
+  __syncthreads();
+  const int t = threadIdx.x % nvec, rg = threadIdx.x / nvec;
+  float gg[E], sg[E] = {}, sb[E] = {}, sx[E] = {};
+  V::unpack(G[t], gg);
+  const U* R = reinterpret_cast<const U*>(dres);
+  U* DX = reinterpret_cast<U*>(dx);
+  constexpr int UR = 4;  // rows in flight per thread
+  for (int rb = r0 + rg; rb < r1; rb += UR * RG) {
+    U pd[UR], pa[UR], pr[UR];
+#pragma unroll
+    for (int k = 0; k < UR; ++k) {
+      const int r = rb + k * RG;
+      if (r < r1) {
+        pd[k] = DY[(int64_t)r * nvec + t];
+        pa[k] = X[(int64_t)r * nvec + t];
+        if (R) pr[k] = R[(int64_t)r * nvec + t];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < UR; ++k) {
+      const int r = rb + k * RG;
+      if (r >= r1) break;
+      const float* q = sstat + 4 * (r - r0);
+      const float s1 = q[0], s2 = q[1], mu = q[2], rs = q[3];
+      float a[E], d[E], rr[E], o[E];
+      V::unpack(pa[k], a);
+      V::unpack(pd[k], d);
+      if (R) V::unpack(pr[k], rr);
+#pragma unroll
+      for (int j = 0; j < E; ++j) {
+        const float xh = (a[j] - mu) * rs;
+        o[j] = rs * (d[j] * gg[j] - s1 - xh * s2) + (R ? rr[j] : 0.f);
+        sg[j] += d[j] * xh;
+        sb[j] += d[j];
+      }
+      const U packed = V::pack(o);
+      DX[(int64_t)r * nvec + t] = packed;
+      if (dxsum) {
+        V::unpack(packed, o);  // as stored
+#pragma unroll
+        for (int j = 0; j < E; ++j) sx[j] += o[j];
+      }
+    }
+  }
+  if (r0 >= r1) return;
+  // row groups 1..RG-1 hand their partials to group 0 through shared memory
+  if (RG > 1) {
+    float* part = sstat + 4 * rows_per;
+    if (rg > 0) {
+      float* my = part + (rg - 1) * 3 * cols;
+#pragma unroll
+      for (int j = 0; j < E; ++j) {
+        my[t * E + j] = sg[j];
+        my[cols + t * E + j] = sb[j];
+        my[2 * cols + t * E + j] = sx[j];
+      }
+    }
+    __syncthreads();
+    if (rg > 0) return;
+#pragma unroll
+    for (int o = 0; o < RG - 1; ++o) {
+      const float* pp = part + o * 3 * cols;
+#pragma unroll
+      for (int j = 0; j < E; ++j) {
+        sg[j] += pp[t * E + j];
+        sb[j] += pp[cols + t * E + j];
+        sx[j] += pp[2 * cols + t * E + j];
+      }
+    }
+  }
+  // one 16-byte vector reduction per 4 columns and output
+#pragma unroll
+  for (int j = 0; j < E; j += 4) {
+    const int c = t * E + j;
+    if (dgamma) red_add_v4(dgamma + c, sg[j], sg[j + 1], sg[j + 2], sg[j + 3]);
+    if (dbeta) red_add_v4(dbeta + c, sb[j], sb[j + 1], sb[j + 2], sb[j + 3]);
+    if (dxsum) red_add_v4(dxsum + c, sx[j], sx[j + 1], sx[j + 2], sx[j + 3]);
+  }
+}
+
 // ---------------------------------------------------------- generic path --
 template <typename T>
 __global__ void ln_fwd_generic(int cols, const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b,
@@ -285,8 +436,40 @@ static int ln_fwd_t(int rows, int cols, const void* x, const void* g, const void
 
 template <typename T>
 static int ln_bwd_t(int rows, int cols, const void* dy, const void* x, const void* g, const float* mean,
-                    const float* rstd, const void* dres, void* dx, float* dgamma, float* dbeta, cudaStream_t st) {
+                    const float* rstd, const void* dres, void* dx, float* dgamma, float* dbeta, float* dxsum,
+                    cudaStream_t st) {
   constexpr int E = Vec<T>::N;
+  const bool al = ((reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(g) |
+                    reinterpret_cast<uintptr_t>(dres) | reinterpret_cast<uintptr_t>(dx) |
+                    reinterpret_cast<uintptr_t>(dgamma) | reinterpret_cast<uintptr_t>(dbeta) |
+                    reinterpret_cast<uintptr_t>(dxsum)) & 15) == 0;
+  const int nvf = cols % (32 * E) == 0 ? cols / (32 * E) : 0;
+  if (al && (nvf == 1 || nvf == 2 || nvf == 4 || nvf == 8 || nvf == 16) && !ln_bwd_unfused()) {
+    // one CTA of rows per SM; fewer CTAs = fewer column reductions at the end
+    const int cps = ln_ctas_per_sm();
+    int rows_per = (rows + cps * num_sms() - 1) / (cps * num_sms());
+    if (rows_per < 4) rows_per = 4;
+    const int grid = (rows + rows_per - 1) / rows_per;
+    const T *DYp = (const T*)dy, *Xp = (const T*)x, *Gp = (const T*)g, *Rp = (const T*)dres;
+    T* DXp = (T*)dx;
+    switch (nvf) {
+#define BP_LNBF(n, rg)                                                                                    \
+  case n: {                                                                                               \
+    const size_t smem = 16 * (size_t)rows_per + 12 * (size_t)cols * (rg - 1);                            \
+    if (smem > 48 * 1024)                                                                                 \
+      BP_CUDA(cudaFuncSetAttribute(ln_bwd_fused<T, n, rg>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                   (int)smem));                                                           \
+    ln_bwd_fused<T, n, rg><<<grid, 32 * n * rg, smem, st>>>(rows, rows_per, DYp, Xp, Gp, mean, rstd, Rp, \
+                                                            DXp, dgamma, dbeta, dxsum);                   \
+    break;                                                                                                \
+  }
+      BP_LNBF(1, 4) BP_LNBF(2, 4) BP_LNBF(4, 4) BP_LNBF(8, 2) BP_LNBF(16, 1)
+#undef BP_LNBF
+    }
+    count_launch();
+    BP_CHECK_LAUNCH("ln_bwd_fused");
+    return BP_OK;
+  }
   const int nv = cols % (32 * E) == 0 ? cols / (32 * E) : 0;
   const T *DY = (const T*)dy, *X = (const T*)x, *G = (const T*)g, *R = (const T*)dres;
   T* DX = (T*)dx;
@@ -302,7 +485,9 @@ static int ln_bwd_t(int rows, int cols, const void* dy, const void* x, const voi
   }
   count_launch();
   BP_CHECK_LAUNCH("ln_bwd_dx");
-  return launch_colred<T, 1>(rows, cols, dy, cols, x, mean, rstd, dgamma, dbeta, st);
+  if (int rc = launch_colred<T, 1>(rows, cols, dy, cols, x, mean, rstd, dgamma, dbeta, st)) return rc;
+  if (dxsum) return launch_colred<T, 0>(rows, cols, dx, cols, nullptr, nullptr, nullptr, dxsum, nullptr, st);
+  return BP_OK;
 }
 
 }  // namespace bp
@@ -320,15 +505,21 @@ extern "C" int bp_layernorm_fwd(int dtype, int rows, int cols, const void* x, co
                          : ln_fwd_t<__nv_bfloat16>(rows, cols, x, gamma, beta, eps, y, mean, rstd, st);
 }
 
-extern "C" int bp_layernorm_bwd(int dtype, int rows, int cols, const void* dy, const void* x, const void* gamma,
-                                const float* mean, const float* rstd, const void* dres, void* dx, float* dgamma,
-                                float* dbeta, void* stream) {
+extern "C" int bp_layernorm_bwd_ex(int dtype, int rows, int cols, const void* dy, const void* x, const void* gamma,
+                                   const float* mean, const float* rstd, const void* dres, void* dx, float* dgamma,
+                                   float* dbeta, float* dx_colsum, void* stream) {
   if (rows <= 0 || cols <= 0) {
     set_error("layernorm_bwd: bad shape");
     return BP_ERR_INVALID;
   }
   cudaStream_t st = (cudaStream_t)stream;
   return dtype == BP_F32
-             ? ln_bwd_t<float>(rows, cols, dy, x, gamma, mean, rstd, dres, dx, dgamma, dbeta, st)
-             : ln_bwd_t<__nv_bfloat16>(rows, cols, dy, x, gamma, mean, rstd, dres, dx, dgamma, dbeta, st);
+             ? ln_bwd_t<float>(rows, cols, dy, x, gamma, mean, rstd, dres, dx, dgamma, dbeta, dx_colsum, st)
+             : ln_bwd_t<__nv_bfloat16>(rows, cols, dy, x, gamma, mean, rstd, dres, dx, dgamma, dbeta, dx_colsum, st);
+}
+
+extern "C" int bp_layernorm_bwd(int dtype, int rows, int cols, const void* dy, const void* x, const void* gamma,
+                                const float* mean, const float* rstd, const void* dres, void* dx, float* dgamma,
+                                float* dbeta, void* stream) {
+  return bp_layernorm_bwd_ex(dtype, rows, cols, dy, x, gamma, mean, rstd, dres, dx, dgamma, dbeta, nullptr, stream);
 }

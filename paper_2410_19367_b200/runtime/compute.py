@@ -114,6 +114,14 @@ class StageCompute:
         return st, out
 
     # ------------------------------------------------------------ backward --
+    def _out_bias_grad(self, i):
+        """fp32 gradient of the output-projection bias of local half-block i
+        (None when i < 0): the column sum of that half-block's output grad."""
+        if i < 0:
+            return None
+        l, half = divmod(self.plan.halfblocks[i], 2)
+        return self.sp.g[f"layers.{l}." + ("attn.proj.b" if half == 0 else "mlp.fc2.b")]
+
     def backward(self, stream, pool: BufferPool, st: Stash, dy, ws):
         """Returns (dx0 or None, buffers to release after this task)."""
         cfg, P, G = self.cfg, self.sp.p, self.sp.g
@@ -127,11 +135,15 @@ class StageCompute:
             ops.gemm(dlogits, P["head.lm.w"], dxf, b_kmajor=False, stream=stream)
             ops.gemm(dlogits, xf, G["head.lm.w"], a_kmajor=False, b_kmajor=False, beta=1.0, stream=stream)
             dy = pool.get((M, h), dt, stream)
+            # the LN backward also sums its dx over rows: that is the output-bias
+            # gradient of the half-block before it (fused, no separate launch)
             ops.layernorm_bwd(dxf, st.xs[-1], P["head.lnf.w"], mean, rstd, dy, G["head.lnf.w"], G["head.lnf.b"],
-                              stream=stream)
+                              dx_colsum=self._out_bias_grad(len(self.plan.halfblocks) - 1), stream=stream)
+            bias_done = bool(self.plan.halfblocks)
             release += [dxf, dy]
         else:
             release.append(dy)
+            bias_done = False
         for i in range(len(self.plan.halfblocks) - 1, -1, -1):
             l, half = divmod(self.plan.halfblocks[i], 2)
             p = f"layers.{l}."
@@ -141,7 +153,8 @@ class StageCompute:
             if half == 0:
                 _, a, mean, rstd, qkv, o, lse = save
                 ops.gemm(dy, o, G[p + "attn.proj.w"], a_kmajor=False, b_kmajor=False, beta=1.0, stream=stream)
-                ops.colsum_acc(dy, G[p + "attn.proj.b"], stream=stream)
+                if not bias_done:
+                    ops.colsum_acc(dy, G[p + "attn.proj.b"], stream=stream)
                 do = pool.get((M, h), dt, stream)
                 ops.gemm(dy, P[p + "attn.proj.w"], do, b_kmajor=False, stream=stream)
                 dqkv = pool.get((M, 3 * h), dt, stream)
@@ -152,12 +165,13 @@ class StageCompute:
                 da = pool.get((M, h), dt, stream)
                 ops.gemm(dqkv, P[p + "attn.qkv.w"], da, b_kmajor=False, stream=stream)
                 ops.layernorm_bwd(da, x, P[p + "ln1.w"], mean, rstd, dx, G[p + "ln1.w"], G[p + "ln1.b"], dres=dy,
-                                  stream=stream)
+                                  dx_colsum=self._out_bias_grad(i - 1), stream=stream)
                 release += [do, dqkv, da]
             else:
                 _, m, mean, rstd, u, g = save
                 ops.gemm(dy, g, G[p + "mlp.fc2.w"], a_kmajor=False, b_kmajor=False, beta=1.0, stream=stream)
-                ops.colsum_acc(dy, G[p + "mlp.fc2.b"], stream=stream)
+                if not bias_done:
+                    ops.colsum_acc(dy, G[p + "mlp.fc2.b"], stream=stream)
                 du = pool.get((M, cfg.ffn), dt, stream)
                 ops.gemm(dy, P[p + "mlp.fc2.w"], du, b_kmajor=False, aux=u, epilogue=EPI_DGELU, stream=stream)
                 ops.gemm(du, m, G[p + "mlp.fc1.w"], a_kmajor=False, b_kmajor=False, beta=1.0, stream=stream)
@@ -165,10 +179,11 @@ class StageCompute:
                 dm = pool.get((M, h), dt, stream)
                 ops.gemm(du, P[p + "mlp.fc1.w"], dm, b_kmajor=False, stream=stream)
                 ops.layernorm_bwd(dm, x, P[p + "ln2.w"], mean, rstd, dx, G[p + "ln2.w"], G[p + "ln2.b"], dres=dy,
-                                  stream=stream)
+                                  dx_colsum=self._out_bias_grad(i - 1), stream=stream)
                 release += [du, dm]
             if i > 0 or self.plan.embed:
                 release.append(dx)
+            bias_done = i > 0
             dy = dx
         if self.plan.embed:
             ops.embed_bwd(st.tokens, dy, G["embed.wte"], G["embed.wpe"], cfg.micro_batch, cfg.seq, stream=stream)

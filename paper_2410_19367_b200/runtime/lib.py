@@ -12,14 +12,14 @@ import threading
 
 __all__ = ["lib", "GemmArgs", "check", "LIB_PATH", "BP_F32", "BP_BF16", "EPI_NONE", "EPI_GELU", "EPI_DGELU",
            "OPT_ATTN_EXACT", "OPT_GEMM_SIMT", "OPT_GEMM_MODE",
-           "OPT_STREAM_K", "OPT_GEMM_WIDE", "OPT_GEMM_DEBUG", "OPT_GEMM_TMA_STORE"]
+           "OPT_STREAM_K", "OPT_GEMM_WIDE", "OPT_GEMM_DEBUG", "OPT_GEMM_TMA_STORE", "OPT_LN_UNFUSED"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "libbitpipe_b200.so")
 
 BP_F32, BP_BF16 = 0, 1
 EPI_NONE, EPI_GELU, EPI_DGELU = 0, 1, 2
 OPT_ATTN_EXACT, OPT_GEMM_SIMT, OPT_GEMM_MODE, OPT_STREAM_K, OPT_GEMM_WIDE = 1, 2, 3, 4, 5
-OPT_GEMM_DEBUG, OPT_GEMM_TMA_STORE = 6, 7
+OPT_GEMM_DEBUG, OPT_GEMM_TMA_STORE, OPT_LN_UNFUSED = 6, 7, 8
 ABI_VERSION = 1
 
 _vp = ctypes.c_void_p
@@ -49,6 +49,7 @@ _SIGS = {
     "bp_gemm": (_i32, [ctypes.POINTER(GemmArgs), _vp]),
     "bp_layernorm_fwd": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _f32, _vp, _vp, _vp, _vp]),
     "bp_layernorm_bwd": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "bp_layernorm_bwd_ex": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "bp_colsum_acc": (_i32, [_i32, _i32, _i32, _vp, _i64, _vp, _vp]),
     "bp_embed_fwd": (_i32, [_i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "bp_embed_bwd": (_i32, [_i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),

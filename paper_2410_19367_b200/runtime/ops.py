@@ -113,10 +113,11 @@ def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
                                  _p(rstd), _s(stream)), "bp_layernorm_fwd")
 
 
-def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, dres=None, stream=None):
+def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, dres=None, dx_colsum=None, stream=None):
+    """dx = dres + dLN(dy); dgamma/dbeta (+ dx_colsum, the column sum of dx) accumulate in fp32."""
     rows, cols = x.shape
-    check(lib().bp_layernorm_bwd(_dt(x), rows, cols, _p(dy), _p(x), _p(gamma), _p(mean), _p(rstd), _p(dres),
-                                 _p(dx), _p(dgamma), _p(dbeta), _s(stream)), "bp_layernorm_bwd")
+    check(lib().bp_layernorm_bwd_ex(_dt(x), rows, cols, _p(dy), _p(x), _p(gamma), _p(mean), _p(rstd), _p(dres),
+                                    _p(dx), _p(dgamma), _p(dbeta), _p(dx_colsum), _s(stream)), "bp_layernorm_bwd")
 
 
 def colsum_acc(x, out, stream=None):

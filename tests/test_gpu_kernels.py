@@ -156,6 +156,44 @@ def test_gemm_tc_matches_simt_bitwise_close():
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("rows,cols", [(64, 64), (300, 1024), (2048, 2048), (17, 100), (5, 256), (2048, 4096)])
+@pytest.mark.parametrize("unfused", [0, 1], ids=["fused", "unfused"])
+def test_layernorm_bwd_colsum(dtype, rows, cols, unfused):
+    """LayerNorm backward with the fused dx column sum (bias grad of the
+    previous half-block), fused and split-kernel paths, vs torch fp32."""
+    from paper_2410_19367_b200.runtime.lib import OPT_LN_UNFUSED
+    x = torch.randn(rows, cols, device="cuda").to(dtype)
+    g = (1 + 0.1 * torch.randn(cols, device="cuda")).to(dtype)
+    b = (0.1 * torch.randn(cols, device="cuda")).to(dtype)
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device="cuda")
+    rstd = torch.empty(rows, device="cuda")
+    ops.layernorm_fwd(x, g, b, y, mean, rstd, eps=1e-5)
+    xr = x.float().requires_grad_(True)
+    gr = g.float().requires_grad_(True)
+    br = b.float().requires_grad_(True)
+    yr = torch.nn.functional.layer_norm(xr, (cols,), gr, br, 1e-5)
+    dy = torch.randn_like(x)
+    dres = torch.randn_like(x)
+    yr.backward(dy.float())
+    dx = torch.empty_like(x)
+    dg = torch.full((cols,), 0.5, device="cuda")
+    db = torch.full((cols,), -0.5, device="cuda")
+    cs = torch.ones(cols, device="cuda")
+    ops.set_option(OPT_LN_UNFUSED, unfused)
+    try:
+        ops.layernorm_bwd(dy, x, g, mean, rstd, dx, dg, db, dres=dres, dx_colsum=cs)
+        torch.cuda.synchronize()
+    finally:
+        ops.set_option(OPT_LN_UNFUSED, 0)
+    tol = 1e-5 if dtype == torch.float32 else 2e-2
+    assert _relerr(dx.float(), xr.grad + dres.float()) < tol
+    assert _relerr(dg, 0.5 + gr.grad) < tol
+    assert _relerr(db, -0.5 + br.grad) < tol
+    assert _relerr(cs, 1 + dx.float().sum(0)) < 1e-5
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("rows,cols", [(64, 64), (300, 1024), (2048, 2048), (17, 100)])
 def test_layernorm(dtype, rows, cols):
     x = torch.randn(rows, cols, device="cuda").to(dtype)
