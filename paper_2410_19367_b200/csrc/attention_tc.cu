@@ -34,11 +34,14 @@ int make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, 
 namespace fat {
 
 #ifdef BP_ATTN_TRACE
-__device__ long long g_trace[64][8];
+__device__ long long g_trace[64][16];
 #define TRACE(it, k) \
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 128 && (it) < 64) g_trace[(it)][(k)] = clock64();
+#define TRACE_MMA(it, k) \
+  if (blockIdx.x == 0 && blockIdx.y == 0 && (it) < 64) g_trace[(it)][(k)] = clock64();
 #else
 #define TRACE(it, k)
+#define TRACE_MMA(it, k)
 #endif
 
 constexpr float kLog2e = 1.4426950408889634f;
@@ -96,16 +99,22 @@ BP_DEV uint64_t mndesc(uint32_t base, int ks, int krows) {
 }
 
 // ============================================================ forward ====
+// 384 threads: warp 0 TMA, warp 1 MMA, warp 2 TMEM allocator, warps 4-11
+// softmax.  Softmax warp w owns TMEM lane quarter (w & 3) -- 32 query rows --
+// and column half hh = (w - 4) >> 2 of every 128-key score tile, so each
+// thread handles 64 scores per tile; the two halves of a row exchange their
+// partial maxima through shared memory (named barrier per lane quarter) and
+// each half rescales / stores its own half of the O columns.
 template <int Dh>
 struct Fwd {
   static constexpr int DC = Dh / 64;
   static constexpr uint32_t TILE = 128 * Dh * 2;
   static constexpr uint32_t PB = 128 * 128 * 2;
-  static constexpr size_t SMEM = 1024 + TILE + 4 * TILE + PB + 512;
+  static constexpr size_t SMEM = 1024 + TILE + 4 * TILE + PB + 2048 + 512;
 };
 
 template <int Dh, bool CAUSAL>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
 fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ o, float* __restrict__ lse, int S,
        int H, float scale_log2) {
   using C = Fwd<Dh>;
@@ -115,7 +124,8 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
   uint8_t* sK[2] = {smem + C::TILE, smem + 3 * C::TILE};
   uint8_t* sV[2] = {smem + 2 * C::TILE, smem + 4 * C::TILE};
   uint8_t* sP = smem + 5 * C::TILE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::PB);
+  float* sX = reinterpret_cast<float*>(sP + C::PB);  // [2 parity][2 halves][128 rows] partial row maxima
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::PB + 2048);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;   // [2]
   uint64_t* kv_empty = bars + 3;  // [2]
@@ -138,9 +148,9 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 128);
+      mbar_init(&s_free[i], 256);
     }
-    mbar_init(p_full, 128);
+    mbar_init(p_full, 256);
     mbar_init(pv_done, 1);
     fence_mbar_init();
   }
@@ -159,6 +169,7 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       for (int j = 0; j < n_kv; ++j) {
         const int st = j & 1;
         mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        TRACE_MMA(32 + j, 10);
         const int krow = b * S + j * 128;
 #pragma unroll
         for (int c = 0; c < C::DC; ++c) {
@@ -180,6 +191,7 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
           const int st = j & 1;
           mbar_wait(&kv_full[st], (j >> 1) & 1);
           mbar_wait(&s_free[st], ((j >> 1) & 1) ^ 1);
+          TRACE_MMA(32 + j, 8);
           tc_fence_after();
           const uint32_t aK = smem_u32(sK[st]);
 #pragma unroll
@@ -190,6 +202,7 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
         if (j >= 1) {
           const int jj = j - 1, st = jj & 1;
           mbar_wait(p_full, jj & 1);
+          TRACE_MMA(32 + jj, 9);
           tc_fence_after();
           const uint32_t aV = smem_u32(sV[st]);
 #pragma unroll
@@ -201,28 +214,38 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       }
     }
   } else if (warp >= 4) {  // ---------------------------------- softmax
-    const int r = (warp - 4) * 32 + lane;
-    const uint32_t tl = tmem + ((uint32_t)((warp - 4) * 32) << 16);
+    const int wq = warp & 3, hh = (warp - 4) >> 2;
+    const int r = wq * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(wq * 32) << 16);
     const uint32_t aP = smem_u32(sP);
+    constexpr int OC = Dh / 64;  // 32-column O chunks per half
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < n_kv; ++j) {
       const int st = j & 1;
+      TRACE(32 + j, 0);
       mbar_wait(&s_full[st], (j >> 1) & 1);
+      TRACE(32 + j, 1);
       tc_fence_after();
-      float s[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tl + st * 128 + c * 32, *reinterpret_cast<float(*)[32]>(s + 32 * c));
+      float s[64];
+      tmem_ld_32x32b_x32_pair(tl + st * 128 + hh * 64, tl + st * 128 + hh * 64 + 32,
+                              *reinterpret_cast<float(*)[32]>(s), *reinterpret_cast<float(*)[32]>(s + 32));
       tc_fence_before();
       mbar_arrive(&s_free[st]);
+      TRACE(32 + j, 2);
       float mx = -INFINITY;
       const bool diag = CAUSAL && (j == qt);
 #pragma unroll
-      for (int i = 0; i < 128; ++i) {
+      for (int i = 0; i < 64; ++i) {
         float v = s[i] * scale_log2;
-        if (diag && i > r) v = -INFINITY;
+        if (diag && hh * 64 + i > r) v = -INFINITY;
         s[i] = v;
         mx = fmaxf(mx, v);
       }
+      float* xs = sX + (j & 1) * 256;
+      xs[hh * 128 + r] = mx;
+      named_bar_sync(1 + wq, 64);
+      mx = fmaxf(mx, xs[(hh ^ 1) * 128 + r]);
+      TRACE(32 + j, 3);
       bool waited = (j == 0);
       if (mx > m_used + 8.f) {
         if (j > 0) {
@@ -231,39 +254,48 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
           tc_fence_after();
           const float f = ex2(m_used - mx);
 #pragma unroll 1
-          for (int c = 0; c < Dh / 32; ++c) {
+          for (int c = 0; c < OC; ++c) {
             float ov[32];
-            tmem_ld_32x32b_x32(tl + 256 + c * 32, ov);
+            const uint32_t ta = tl + 256 + (hh * OC + c) * 32;
+            tmem_ld_32x32b_x32(ta, ov);
 #pragma unroll
             for (int i = 0; i < 32; ++i) ov[i] *= f;
-            tmem_st_32x32b_x32(tl + 256 + c * 32, ov);
+            tmem_st_32x32b_x32(ta, ov);
           }
           l *= f;
         }
         m_used = mx;
       }
+      TRACE(32 + j, 4);
       float lsum = 0.f;
 #pragma unroll
-      for (int i = 0; i < 128; ++i) {
+      for (int i = 0; i < 64; ++i) {
         s[i] = ex2(s[i] - m_used);
         lsum += s[i];
       }
       l += lsum;
+      TRACE(32 + j, 5);
       if (!waited) mbar_wait(pv_done, (j - 1) & 1);
+      TRACE(32 + j, 6);
 #pragma unroll
-      for (int u = 0; u < 16; ++u) st_shared_v4(aP + kmaj_off(r, u, 128), pack8(s + 8 * u));
+      for (int u = 0; u < 8; ++u) st_shared_v4(aP + kmaj_off(r, hh * 8 + u, 128), pack8(s + 8 * u));
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(p_full);
+      TRACE(32 + j, 7);
     }
-    // epilogue: O / l
+    // epilogue: O / l (l = sum of both halves' partial sums)
+    float* xs = sX + (n_kv & 1) * 256;
+    xs[hh * 128 + r] = l;
+    named_bar_sync(1 + wq, 64);
+    l += xs[(hh ^ 1) * 128 + r];
     mbar_wait(pv_done, (n_kv - 1) & 1);
     tc_fence_after();
     const int q = qt * 128 + r;
     const float inv = l > 0.f ? 1.f / l : 0.f;
     __nv_bfloat16* orow = o + ((int64_t)b * S + q) * HD + h * Dh;
 #pragma unroll 1
-    for (int c = 0; c < Dh / 32; ++c) {
+    for (int c = hh * OC; c < (hh + 1) * OC; ++c) {
       float ov[32];
       tmem_ld_32x32b_x32(tl + 256 + c * 32, ov);
 #pragma unroll
@@ -271,7 +303,7 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
 #pragma unroll
       for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(orow + c * 32 + 8 * u) = pack8(ov + 8 * u);
     }
-    lse[((int64_t)b * H + h) * S + q] = (m_used + log2f(l)) * kLn2;
+    if (hh == 0) lse[((int64_t)b * H + h) * S + q] = (m_used + log2f(l)) * kLn2;
   }
   tc_fence_before();
   __syncthreads();
@@ -279,40 +311,54 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
 }
 
 // =================================================== backward: dK, dV ====
+// CTA = 128 keys, 384 threads.  Two compute warpgroups ping-pong over the
+// 64-query tiles (warps 4-7 take even tiles, warps 8-11 odd ones), so one
+// group's exp / dS math overlaps the other's and the tensor pipe always has
+// the next S^T / dP^T pair queued: S^T / dP^T are double-buffered in TMEM and
+// P^T / dS^T in shared memory.  Q / dO / LSE / delta stream through a
+// QST-deep TMA ring.
 template <int Dh>
 struct Dkdv {
   static constexpr int DC = Dh / 64;
+  static constexpr int QST = 3;
   static constexpr uint32_t KT = 128 * Dh * 2;  // K / V tile (128 keys)
   static constexpr uint32_t QT = 64 * Dh * 2;   // Q / dO tile (64 queries)
   static constexpr uint32_t PB = 128 * 64 * 2;  // P^T / dS^T tile
-  static constexpr size_t SMEM = 1024 + 2 * KT + 4 * QT + 2 * PB + 2 * 512 + 512;
+  static constexpr size_t SMEM = 1024 + 2 * KT + QST * 2 * QT + 4 * PB + QST * 512 + 512;
 };
 
+BP_DEV float4 lds4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+
 template <int Dh, bool CAUSAL>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
 dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUtensorMap map_q,
         const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse, const float* __restrict__ delta,
         __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale, float scale_log2) {
   using C = Dkdv<Dh>;
+  constexpr int QST = C::QST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = smem;
   uint8_t* sV = smem + C::KT;
-  uint8_t* sQ[2] = {smem + 2 * C::KT, smem + 2 * C::KT + 2 * C::QT};
-  uint8_t* sO[2] = {smem + 2 * C::KT + C::QT, smem + 2 * C::KT + 3 * C::QT};
-  uint8_t* sP = smem + 2 * C::KT + 4 * C::QT;
-  uint8_t* sD = sP + C::PB;
-  float* sL[2] = {reinterpret_cast<float*>(sD + C::PB), reinterpret_cast<float*>(sD + C::PB + 512)};
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + C::PB + 1024);
+  uint8_t* sQ0 = smem + 2 * C::KT;     // stage s: Q at sQ0 + 2 s QT, dO right after
+  uint8_t* sPD = sQ0 + QST * 2 * C::QT;  // buffer g: P^T at sPD + 2 g PB, dS^T right after
+  float* sL0 = reinterpret_cast<float*>(sPD + 4 * C::PB);  // stage s: 64 lse then 64 delta
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sPD + 4 * C::PB + QST * 512);
   uint64_t* kv_full = bars;
-  uint64_t* q_full = bars + 1;   // [2]
-  uint64_t* q_empty = bars + 3;  // [2]
-  uint64_t* sdp_full = bars + 5;
-  uint64_t* sdp_free = bars + 6;
-  uint64_t* p_full = bars + 7;
-  uint64_t* mm_done = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
-  // TMEM columns: S^T [0,64), dP^T [64,128), dV [128,128+Dh), dK [128+Dh, 128+2Dh)
+  uint64_t* q_full = bars + 1;          // [QST]
+  uint64_t* q_empty = bars + 1 + QST;   // [QST]
+  uint64_t* sdp_full = bars + 1 + 2 * QST;  // [2]
+  uint64_t* sdp_free = sdp_full + 2;        // [2]
+  uint64_t* p_full = sdp_full + 4;          // [2]
+  uint64_t* mm_done = sdp_full + 6;         // [2]
+  uint64_t* all_done = sdp_full + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sdp_full + 9);
+  // TMEM columns: buffer g: S^T [128g, 128g+64), dP^T [128g+64, 128g+128);
+  //               dV [256, 256+Dh), dK [256+Dh, 256+2Dh)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bh = blockIdx.x, kt = blockIdx.y;
   const int b = bh / H, h = bh % H;
@@ -328,14 +374,17 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
   }
   if (warp == 1 && lane == 0) {
     mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < QST; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
     }
-    mbar_init(sdp_full, 1);
-    mbar_init(sdp_free, 128);
-    mbar_init(p_full, 128);
-    mbar_init(mm_done, 1);
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(&sdp_full[g], 1);
+      mbar_init(&sdp_free[g], 128);
+      mbar_init(&p_full[g], 128);
+      mbar_init(&mm_done[g], 1);
+    }
+    mbar_init(all_done, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -354,17 +403,19 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
       }
       mbar_expect_tx(kv_full, 2 * C::KT);
       for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1, qi = q0 + it;
-        mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
+        const int st = it % QST, qi = q0 + it;
+        mbar_wait(&q_empty[st], ((it / QST) & 1) ^ 1);
+        TRACE_MMA(it, 12);
         const int qrow = b * S + qi * 64;
+        uint8_t* sq = sQ0 + st * 2 * C::QT;
 #pragma unroll
         for (int c = 0; c < C::DC; ++c) {
-          tma_load_2d(sQ[st] + c * 8192, &map_q, h * Dh + c * 64, qrow, &q_full[st]);
-          tma_load_2d(sO[st] + c * 8192, &map_do, h * Dh + c * 64, qrow, &q_full[st]);
+          tma_load_2d(sq + c * 8192, &map_q, h * Dh + c * 64, qrow, &q_full[st]);
+          tma_load_2d(sq + C::QT + c * 8192, &map_do, h * Dh + c * 64, qrow, &q_full[st]);
         }
         const int64_t lrow = ((int64_t)b * H + h) * S + qi * 64;
-        bulk_load(sL[st], lse + lrow, 256, &q_full[st]);
-        bulk_load(sL[st] + 64, delta + lrow, 256, &q_full[st]);
+        bulk_load(sL0 + st * 128, lse + lrow, 256, &q_full[st]);
+        bulk_load(sL0 + st * 128 + 64, delta + lrow, 256, &q_full[st]);
         mbar_expect_tx(&q_full[st], 2 * C::QT + 512);
       }
     }
@@ -372,99 +423,125 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
     if (lane == 0) {  // ------------------------------------ MMA issuer
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, 64, false, false);  // S^T, dP^T: M=keys, N=64 q
       constexpr uint32_t idesc_g = umma_idesc_bf16(128, Dh, false, true);   // dV, dK: B MN-major
-      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aP = smem_u32(sP), aD = smem_u32(sD);
+      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
       mbar_wait(kv_full, 0);
       tc_fence_after();
-      for (int it = 0; it <= n_it; ++it) {
-        if (it < n_it) {
-          const int st = it & 1;
-          mbar_wait(&q_full[st], (it >> 1) & 1);
-          mbar_wait(sdp_free, (it & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t aQ = smem_u32(sQ[st]), aO = smem_u32(sO[st]);
+      auto issue_sdp = [&](int it) {
+        const int st = it % QST, g = it & 1;
+        TRACE_MMA(it, 8);
+        mbar_wait(&q_full[st], (it / QST) & 1);
+        TRACE_MMA(it, 9);
+        mbar_wait(&sdp_free[g], ((it >> 1) & 1) ^ 1);
+        TRACE_MMA(it, 10);
+        tc_fence_after();
+        const uint32_t aQ = smem_u32(sQ0 + st * 2 * C::QT), aO = aQ + C::QT;
 #pragma unroll
-          for (int ks = 0; ks < Dh / 16; ++ks) {
-            tc_mma_f16(tmem + 0, kdesc(aK, ks, 128), kdesc(aQ, ks, 64), idesc_s, ks > 0);
-            tc_mma_f16(tmem + 64, kdesc(aV, ks, 128), kdesc(aO, ks, 64), idesc_s, ks > 0);
-          }
-          tc_commit(sdp_full);
+        for (int ks = 0; ks < Dh / 16; ++ks) {
+          tc_mma_f16(tmem + g * 128, kdesc(aK, ks, 128), kdesc(aQ, ks, 64), idesc_s, ks > 0);
+          tc_mma_f16(tmem + g * 128 + 64, kdesc(aV, ks, 128), kdesc(aO, ks, 64), idesc_s, ks > 0);
         }
-        if (it >= 1) {
-          const int jj = it - 1, st = jj & 1;
-          mbar_wait(p_full, jj & 1);
-          tc_fence_after();
-          const uint32_t aQ = smem_u32(sQ[st]), aO = smem_u32(sO[st]);
+        tc_commit(&sdp_full[g]);
+      };
+      issue_sdp(0);
+      if (n_it > 1) issue_sdp(1);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it % QST, g = it & 1;
+        mbar_wait(&p_full[g], (it >> 1) & 1);
+        TRACE_MMA(it, 11);
+        tc_fence_after();
+        const uint32_t aQ = smem_u32(sQ0 + st * 2 * C::QT), aO = aQ + C::QT;
+        const uint32_t aP = smem_u32(sPD + 2 * g * C::PB), aD = aP + C::PB;
 #pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {  // 64 queries / 16
-            tc_mma_f16(tmem + 128, kdesc(aP, ks, 128), mndesc(aO, ks, 64), idesc_g, (jj > 0 || ks > 0));
-            tc_mma_f16(tmem + 128 + Dh, kdesc(aD, ks, 128), mndesc(aQ, ks, 64), idesc_g, (jj > 0 || ks > 0));
-          }
-          tc_commit(mm_done);
-          tc_commit(&q_empty[st]);
+        for (int ks = 0; ks < 4; ++ks) {  // 64 queries / 16
+          tc_mma_f16(tmem + 256, kdesc(aP, ks, 128), mndesc(aO, ks, 64), idesc_g, (it > 0 || ks > 0));
+          tc_mma_f16(tmem + 256 + Dh, kdesc(aD, ks, 128), mndesc(aQ, ks, 64), idesc_g, (it > 0 || ks > 0));
         }
+        tc_commit(&mm_done[g]);
+        tc_commit(&q_empty[st]);
+        if (it + 2 < n_it) issue_sdp(it + 2);
       }
+      tc_commit(all_done);
     }
   } else if (warp >= 4) {  // -------------------------- P^T / dS^T rows
-    const int r = (warp - 4) * 32 + lane;  // key row in the tile
+    const int wq = warp & 3, g = (warp - 4) >> 2;
+    const int r = wq * 32 + lane;  // key row in the tile
     const int key = kt * 128 + r;
-    const uint32_t tl = tmem + ((uint32_t)((warp - 4) * 32) << 16);
-    const uint32_t aP = smem_u32(sP), aD = smem_u32(sD);
-    for (int it = 0; it < n_it; ++it) {
-      const int st = it & 1, qi = q0 + it;
+    const uint32_t tl = tmem + ((uint32_t)(wq * 32) << 16) + g * 128;
+    const uint32_t aP = smem_u32(sPD + 2 * g * C::PB), aD = aP + C::PB;
+    for (int it = g; it < n_it; it += 2) {
+      const int st = it % QST, qi = q0 + it, u = it >> 1;
       TRACE(it, 0);
-      mbar_wait(&q_full[st], (it >> 1) & 1);  // lse / delta of this tile are in smem
+      mbar_wait(&q_full[st], (it / QST) & 1);  // lse / delta of this tile are in smem
       TRACE(it, 1);
-      mbar_wait(sdp_full, it & 1);
+      mbar_wait(&sdp_full[g], u & 1);
       TRACE(it, 2);
       tc_fence_after();
-      float sv[64], dp[64];
-      tmem_ld_32x32b_x32(tl + 0, *reinterpret_cast<float(*)[32]>(sv));
-      tmem_ld_32x32b_x32(tl + 32, *reinterpret_cast<float(*)[32]>(sv + 32));
-      tmem_ld_32x32b_x32(tl + 64, *reinterpret_cast<float(*)[32]>(dp));
-      tmem_ld_32x32b_x32(tl + 96, *reinterpret_cast<float(*)[32]>(dp + 32));
-      TRACE(it, 3);
-      tc_fence_before();
-      mbar_arrive(sdp_free);
-      const uint32_t aL = smem_u32(sL[st]);
-      const bool diag = CAUSAL && qi * 64 < key;  // some query of this tile precedes the key
+      const uint32_t aL = smem_u32(sL0 + st * 128);
+#pragma unroll 1
+      for (int hf = 0; hf < 2; ++hf) {
+        float sv[32], dp[32];
+        tmem_ld_32x32b_x32_pair(tl + hf * 32, tl + 64 + hf * 32, sv, dp);
+        if (hf == 1) {
+          tc_fence_before();
+          mbar_arrive(&sdp_free[g]);
+        }
+        TRACE(it, 3);
+        const int qb = qi * 64 + hf * 32;
+        if (CAUSAL && qb < key) {  // some query of this half precedes the key
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        const int q = qi * 64 + i;
-        float p = ex2(fmaf(sv[i], scale_log2, -lds(aL + 4 * i) * kLog2e));
-        if (diag && q < key) p = 0.f;
-        sv[i] = p;
-        dp[i] = p * (dp[i] - lds(aL + 256 + 4 * i));
-      }
-      TRACE(it, 4);
-      if (it > 0) mbar_wait(mm_done, (it - 1) & 1);
-      TRACE(it, 5);
+          for (int k = 0; k < 8; ++k) {
+            const float4 l4 = lds4(aL + 4 * (hf * 32 + 4 * k)), d4 = lds4(aL + 256 + 4 * (hf * 32 + 4 * k));
+            const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dl[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        st_shared_v4(aP + kmaj_off(r, u, 128), pack8(sv + 8 * u));
-        st_shared_v4(aD + kmaj_off(r, u, 128), pack8(dp + 8 * u));
+            for (int e = 0; e < 4; ++e) {
+              const int i = 4 * k + e;
+              float p = ex2(fmaf(sv[i], scale_log2, -lv[e] * kLog2e));
+              p = qb + i < key ? 0.f : p;
+              sv[i] = p;
+              dp[i] = p * (dp[i] - dl[e]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float4 l4 = lds4(aL + 4 * (hf * 32 + 4 * k)), d4 = lds4(aL + 256 + 4 * (hf * 32 + 4 * k));
+            const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dl[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int i = 4 * k + e;
+              const float p = ex2(fmaf(sv[i], scale_log2, -lv[e] * kLog2e));
+              sv[i] = p;
+              dp[i] = p * (dp[i] - dl[e]);
+            }
+          }
+        }
+        TRACE(it, 4);
+        if (hf == 0 && u > 0) mbar_wait(&mm_done[g], (u - 1) & 1);  // dV/dK(it - 2) read this buffer
+        TRACE(it, 5);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          st_shared_v4(aP + kmaj_off(r, hf * 4 + v, 128), pack8(sv + 8 * v));
+          st_shared_v4(aD + kmaj_off(r, hf * 4 + v, 128), pack8(dp + 8 * v));
+        }
       }
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[g]);
       TRACE(it, 6);
     }
-    // epilogue: dV, dK (scaled) -> dqkv
-    if (n_it > 0) mbar_wait(mm_done, (n_it - 1) & 1);
+    // epilogue: dV, dK (scaled) -> dqkv; group g writes 32-column chunks g, g+2, ...
+    mbar_wait(all_done, 0);
     tc_fence_after();
+    const uint32_t te = tmem + ((uint32_t)(wq * 32) << 16) + 256;
     __nv_bfloat16* dkrow = dqkv + ((int64_t)b * S + key) * 3 * HD + HD + h * Dh;
     __nv_bfloat16* dvrow = dkrow + HD;
 #pragma unroll 1
-    for (int c = 0; c < Dh / 32; ++c) {
+    for (int c = g; c < Dh / 32; c += 2) {
       float v[32];
-      if (n_it > 0) {
-        tmem_ld_32x32b_x32(tl + 128 + c * 32, v);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = 0.f;
-      }
+      tmem_ld_32x32b_x32(te + c * 32, v);
 #pragma unroll
       for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(dvrow + c * 32 + 8 * u) = pack8(v + 8 * u);
-      if (n_it > 0) tmem_ld_32x32b_x32(tl + 128 + Dh + c * 32, v);
+      tmem_ld_32x32b_x32(te + Dh + c * 32, v);
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] *= scale;
 #pragma unroll
@@ -477,38 +554,43 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
 }
 
 // ========================================================= backward: dQ ====
+// CTA = 128 queries, 384 threads; two compute warpgroups ping-pong over the
+// 64-key tiles exactly as in dkdv_tc (S / dP double-buffered in TMEM, dS in
+// shared memory); K / V stream through a KST-deep ring.
 template <int Dh>
 struct Dq {
   static constexpr int DC = Dh / 64;
+  static constexpr int KST = 4;
   static constexpr uint32_t QT = 128 * Dh * 2;  // Q / dO tile (128 queries)
   static constexpr uint32_t KT = 64 * Dh * 2;   // K / V tile (64 keys)
   static constexpr uint32_t DB = 128 * 64 * 2;  // dS tile
-  static constexpr size_t SMEM = 1024 + 2 * QT + 4 * KT + DB + 512;
+  static constexpr size_t SMEM = 1024 + 2 * QT + KST * 2 * KT + 2 * DB + 512;
 };
 
 template <int Dh, bool CAUSAL>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
 dq_tc(const __grid_constant__ CUtensorMap map_q128, const __grid_constant__ CUtensorMap map_kv64,
       const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse, const float* __restrict__ delta,
       __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale, float scale_log2) {
   using C = Dq<Dh>;
+  constexpr int KST = C::KST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sO = smem + C::QT;
-  uint8_t* sK[2] = {smem + 2 * C::QT, smem + 2 * C::QT + 2 * C::KT};
-  uint8_t* sV[2] = {smem + 2 * C::QT + C::KT, smem + 2 * C::QT + 3 * C::KT};
-  uint8_t* sD = smem + 2 * C::QT + 4 * C::KT;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + C::DB);
+  uint8_t* sK0 = smem + 2 * C::QT;  // stage s: K at sK0 + 2 s KT, V right after
+  uint8_t* sD0 = sK0 + KST * 2 * C::KT;  // buffer g: dS at sD0 + g DB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sD0 + 2 * C::DB);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* sdp_full = bars + 5;
-  uint64_t* sdp_free = bars + 6;
-  uint64_t* p_full = bars + 7;
-  uint64_t* mm_done = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
-  // TMEM: S [0,64), dP [64,128), dQ [128, 128+Dh)
+  uint64_t* kv_full = bars + 1;          // [KST]
+  uint64_t* kv_empty = bars + 1 + KST;   // [KST]
+  uint64_t* sdp_full = bars + 1 + 2 * KST;  // [2]
+  uint64_t* sdp_free = sdp_full + 2;        // [2]
+  uint64_t* p_full = sdp_full + 4;          // [2]
+  uint64_t* mm_done = sdp_full + 6;         // [2]
+  uint64_t* all_done = sdp_full + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sdp_full + 9);
+  // TMEM: buffer g: S [128g, 128g+64), dP [128g+64, 128g+128); dQ [256, 256+Dh)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bh = blockIdx.x, qt = gridDim.y - 1 - blockIdx.y;
   const int b = bh / H, h = bh % H;
@@ -522,17 +604,20 @@ dq_tc(const __grid_constant__ CUtensorMap map_q128, const __grid_constant__ CUte
   }
   if (warp == 1 && lane == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < KST; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
-    mbar_init(sdp_full, 1);
-    mbar_init(sdp_free, 128);
-    mbar_init(p_full, 128);
-    mbar_init(mm_done, 1);
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(&sdp_full[g], 1);
+      mbar_init(&sdp_free[g], 128);
+      mbar_init(&p_full[g], 128);
+      mbar_init(&mm_done[g], 1);
+    }
+    mbar_init(all_done, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<256>(tmem_slot);
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -548,13 +633,14 @@ dq_tc(const __grid_constant__ CUtensorMap map_q128, const __grid_constant__ CUte
       }
       mbar_expect_tx(q_full, 2 * C::QT);
       for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1;
-        mbar_wait(&kv_empty[st], ((it >> 1) & 1) ^ 1);
+        const int st = it % KST;
+        mbar_wait(&kv_empty[st], ((it / KST) & 1) ^ 1);
         const int krow = b * S + it * 64;
+        uint8_t* sk = sK0 + st * 2 * C::KT;
 #pragma unroll
         for (int c = 0; c < C::DC; ++c) {
-          tma_load_2d(sK[st] + c * 8192, &map_kv64, HD + h * Dh + c * 64, krow, &kv_full[st]);
-          tma_load_2d(sV[st] + c * 8192, &map_kv64, 2 * HD + h * Dh + c * 64, krow, &kv_full[st]);
+          tma_load_2d(sk + c * 8192, &map_kv64, HD + h * Dh + c * 64, krow, &kv_full[st]);
+          tma_load_2d(sk + C::KT + c * 8192, &map_kv64, 2 * HD + h * Dh + c * 64, krow, &kv_full[st]);
         }
         mbar_expect_tx(&kv_full[st], 2 * C::KT);
       }
@@ -563,74 +649,89 @@ dq_tc(const __grid_constant__ CUtensorMap map_q128, const __grid_constant__ CUte
     if (lane == 0) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, 64, false, false);
       constexpr uint32_t idesc_q = umma_idesc_bf16(128, Dh, false, true);
-      const uint32_t aQ = smem_u32(sQ), aO = smem_u32(sO), aD = smem_u32(sD);
+      const uint32_t aQ = smem_u32(sQ), aO = smem_u32(sO);
       mbar_wait(q_full, 0);
       tc_fence_after();
-      for (int it = 0; it <= n_it; ++it) {
-        if (it < n_it) {
-          const int st = it & 1;
-          mbar_wait(&kv_full[st], (it >> 1) & 1);
-          mbar_wait(sdp_free, (it & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t aK = smem_u32(sK[st]), aV = smem_u32(sV[st]);
+      auto issue_sdp = [&](int it) {
+        const int st = it % KST, g = it & 1;
+        mbar_wait(&kv_full[st], (it / KST) & 1);
+        mbar_wait(&sdp_free[g], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t aK = smem_u32(sK0 + st * 2 * C::KT), aV = aK + C::KT;
 #pragma unroll
-          for (int ks = 0; ks < Dh / 16; ++ks) {
-            tc_mma_f16(tmem + 0, kdesc(aQ, ks, 128), kdesc(aK, ks, 64), idesc_s, ks > 0);
-            tc_mma_f16(tmem + 64, kdesc(aO, ks, 128), kdesc(aV, ks, 64), idesc_s, ks > 0);
-          }
-          tc_commit(sdp_full);
+        for (int ks = 0; ks < Dh / 16; ++ks) {
+          tc_mma_f16(tmem + g * 128, kdesc(aQ, ks, 128), kdesc(aK, ks, 64), idesc_s, ks > 0);
+          tc_mma_f16(tmem + g * 128 + 64, kdesc(aO, ks, 128), kdesc(aV, ks, 64), idesc_s, ks > 0);
         }
-        if (it >= 1) {
-          const int jj = it - 1, st = jj & 1;
-          mbar_wait(p_full, jj & 1);
-          tc_fence_after();
-          const uint32_t aK = smem_u32(sK[st]);
+        tc_commit(&sdp_full[g]);
+      };
+      issue_sdp(0);
+      if (n_it > 1) issue_sdp(1);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it % KST, g = it & 1;
+        mbar_wait(&p_full[g], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t aK = smem_u32(sK0 + st * 2 * C::KT), aD = smem_u32(sD0 + g * C::DB);
 #pragma unroll
-          for (int ks = 0; ks < 4; ++ks)
-            tc_mma_f16(tmem + 128, kdesc(aD, ks, 128), mndesc(aK, ks, 64), idesc_q, (jj > 0 || ks > 0));
-          tc_commit(mm_done);
-          tc_commit(&kv_empty[st]);
-        }
+        for (int ks = 0; ks < 4; ++ks)
+          tc_mma_f16(tmem + 256, kdesc(aD, ks, 128), mndesc(aK, ks, 64), idesc_q, (it > 0 || ks > 0));
+        tc_commit(&mm_done[g]);
+        tc_commit(&kv_empty[st]);
+        if (it + 2 < n_it) issue_sdp(it + 2);
       }
+      tc_commit(all_done);
     }
   } else if (warp >= 4) {
-    const int r = (warp - 4) * 32 + lane;
+    const int wq = warp & 3, g = (warp - 4) >> 2;
+    const int r = wq * 32 + lane;
     const int q = qt * 128 + r;
-    const uint32_t tl = tmem + ((uint32_t)((warp - 4) * 32) << 16);
-    const uint32_t aD = smem_u32(sD);
+    const uint32_t tl = tmem + ((uint32_t)(wq * 32) << 16) + g * 128;
+    const uint32_t aD = smem_u32(sD0 + g * C::DB);
     const int64_t li = ((int64_t)b * H + h) * S + q;
     const float lse2 = lse[li] * kLog2e, dl = delta[li];
-    for (int it = 0; it < n_it; ++it) {
-      mbar_wait(sdp_full, it & 1);
+    for (int it = g; it < n_it; it += 2) {
+      const int u = it >> 1;
+      mbar_wait(&sdp_full[g], u & 1);
       tc_fence_after();
-      float sv[64], dp[64];
-      tmem_ld_32x32b_x32(tl + 0, *reinterpret_cast<float(*)[32]>(sv));
-      tmem_ld_32x32b_x32(tl + 32, *reinterpret_cast<float(*)[32]>(sv + 32));
-      tmem_ld_32x32b_x32(tl + 64, *reinterpret_cast<float(*)[32]>(dp));
-      tmem_ld_32x32b_x32(tl + 96, *reinterpret_cast<float(*)[32]>(dp + 32));
-      tc_fence_before();
-      mbar_arrive(sdp_free);
-      const bool diag = CAUSAL && (it * 64 + 63 > q);
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        float p = ex2(fmaf(sv[i], scale_log2, -lse2));
-        if (diag && it * 64 + i > q) p = 0.f;
-        dp[i] = p * (dp[i] - dl);
+      for (int hf = 0; hf < 2; ++hf) {
+        float sv[32], dp[32];
+        tmem_ld_32x32b_x32_pair(tl + hf * 32, tl + 64 + hf * 32, sv, dp);
+        if (hf == 1) {
+          tc_fence_before();
+          mbar_arrive(&sdp_free[g]);
+        }
+        const int kb = it * 64 + hf * 32;
+        if (CAUSAL && kb + 31 > q) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            float p = ex2(fmaf(sv[i], scale_log2, -lse2));
+            p = kb + i > q ? 0.f : p;
+            dp[i] = p * (dp[i] - dl);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float p = ex2(fmaf(sv[i], scale_log2, -lse2));
+            dp[i] = p * (dp[i] - dl);
+          }
+        }
+        if (hf == 0 && u > 0) mbar_wait(&mm_done[g], (u - 1) & 1);  // dQ(it - 2) read this buffer
+#pragma unroll
+        for (int v = 0; v < 4; ++v) st_shared_v4(aD + kmaj_off(r, hf * 4 + v, 128), pack8(dp + 8 * v));
       }
-      if (it > 0) mbar_wait(mm_done, (it - 1) & 1);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) st_shared_v4(aD + kmaj_off(r, u, 128), pack8(dp + 8 * u));
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[g]);
     }
-    mbar_wait(mm_done, (n_it - 1) & 1);
+    mbar_wait(all_done, 0);
     tc_fence_after();
+    const uint32_t te = tmem + ((uint32_t)(wq * 32) << 16) + 256;
     __nv_bfloat16* dqrow = dqkv + ((int64_t)b * S + q) * 3 * HD + h * Dh;
 #pragma unroll 1
-    for (int c = 0; c < Dh / 32; ++c) {
+    for (int c = g; c < Dh / 32; c += 2) {
       float v[32];
-      tmem_ld_32x32b_x32(tl + 128 + c * 32, v);
+      tmem_ld_32x32b_x32(te + c * 32, v);
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] *= scale;
 #pragma unroll
@@ -639,7 +740,7 @@ dq_tc(const __grid_constant__ CUtensorMap map_q128, const __grid_constant__ CUte
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_dealloc<256>(tmem);
+  if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
 template <int Dh>
@@ -676,7 +777,7 @@ static int fwd(int B, int S, int H, float scale, const void* qkv, void* o, float
     if (int rc = set_smem(k, Fwd<Dh>::SMEM)) return rc;
     once = true;
   }
-  k<<<dim3(B * H, S / 128), 256, Fwd<Dh>::SMEM, st>>>(m, (__nv_bfloat16*)o, lse, S, H, scale * kLog2e);
+  k<<<dim3(B * H, S / 128), 384, Fwd<Dh>::SMEM, st>>>(m, (__nv_bfloat16*)o, lse, S, H, scale * kLog2e);
   count_launch();
   BP_CHECK_LAUNCH("attn_fwd_tc");
   return BP_OK;
@@ -707,10 +808,10 @@ static int bwd(int B, int S, int H, float scale, const void* qkv, const void* o,
     once = true;
   }
   const float sl2 = scale * kLog2e;
-  k1<<<dim3(B * H, S / 128), 256, Dkdv<Dh>::SMEM, st>>>(kv128, q64, do64, lse, delta, (__nv_bfloat16*)dqkv, S, H,
+  k1<<<dim3(B * H, S / 128), 384, Dkdv<Dh>::SMEM, st>>>(kv128, q64, do64, lse, delta, (__nv_bfloat16*)dqkv, S, H,
                                                          scale, sl2);
   count_launch();
-  k2<<<dim3(B * H, S / 128), 256, Dq<Dh>::SMEM, st>>>(q128, kv64, do128, lse, delta, (__nv_bfloat16*)dqkv, S, H,
+  k2<<<dim3(B * H, S / 128), 384, Dq<Dh>::SMEM, st>>>(q128, kv64, do128, lse, delta, (__nv_bfloat16*)dqkv, S, H,
                                                        scale, sl2);
   count_launch();
   BP_CHECK_LAUNCH("attn_bwd_tc");
@@ -720,9 +821,9 @@ static int bwd(int B, int S, int H, float scale, const void* qkv, const void* o,
 }  // namespace fat
 
 // Debug aid (BP_ATTN_TRACE builds): copy the dK/dV softmax-warp timestamps.
-extern "C" int bp_attn_trace_dump(long long* host, int n) {
+extern "C" __attribute__((visibility("default"))) int bp_attn_trace_dump(long long* host, int n) {
 #ifdef BP_ATTN_TRACE
-  return cudaMemcpyFromSymbol(host, fat::g_trace, sizeof(long long) * (n < 512 ? n : 512)) == cudaSuccess ? 0 : 2;
+  return cudaMemcpyFromSymbol(host, fat::g_trace, sizeof(long long) * (n < 1024 ? n : 1024)) == cudaSuccess ? 0 : 2;
 #else
   (void)host; (void)n;
   return 3;

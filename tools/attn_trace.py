@@ -1,5 +1,7 @@
-"""Per-iteration timestamps of the dK/dV softmax warp (CTA 0,0) from a
-BP_ATTN_TRACE build (tools/libbitpipe_trace.so)."""
+"""Per-iteration timestamps of the dK/dV kernel (CTA 0,0) from a
+BP_ATTN_TRACE build (tools/libbitpipe_trace.so): compute warp phases, the
+MMA warp's issue points and the producer's Q-tile issue, all relative to the
+compute warp's iteration start."""
 import ctypes
 import math
 import os
@@ -25,15 +27,26 @@ torch.cuda.synchronize()
 h = L.lib()
 fn = h.bp_attn_trace_dump
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = (ctypes.c_longlong * 512)()
-print("rc", fn(buf, 512))
-t = [[buf[i * 8 + k] for k in range(8)] for i in range(64)]
-base = t[0][0]
-names = ["q_full wait", "sdp_full wait", "tmem ld", "compute", "mm_done wait", "st+arrive", "->next"]
-print("iter  " + " ".join(f"{n:>13s}" for n in names))
+buf = (ctypes.c_longlong * 1024)()
+print("rc", fn(buf, 1024))
+t = [[buf[i * 16 + k] for k in range(16)] for i in range(64)]
+names = ["q_full", "sdp_full", "tmem_ld", "compute", "mm_done", "st+arr", "->next"]
+print("iter " + " ".join(f"{n:>8s}" for n in names) + " | rel. to iter start: mma_top q_ok sdp_iss dvdk_iss prod_q")
 for i in range(32):
     row = t[i]
     if row[0] == 0:
         break
     d = [row[k + 1] - row[k] for k in range(6)] + [(t[i + 1][0] - row[6]) if i + 1 < 64 and t[i + 1][0] else 0]
-    print(f"{i:4d}  " + " ".join(f"{x:13d}" for x in d))
+    rel = [row[k] - row[0] if row[k] else 0 for k in (8, 9, 10, 11, 12)]
+    print(f"{i:4d} " + " ".join(f"{x:8d}" for x in d) + " | " + " ".join(f"{x:8d}" for x in rel))
+
+# forward kernel, CTA (0,0) = last query tile (16 key tiles), rows 32..47
+names = ["s_full", "ld+arr", "max+xchg", "rescale", "exp+sum", "pv_wait", "st+arr", "->next"]
+print("fwd  " + " ".join(f"{n:>8s}" for n in names) + " | rel: S_iss PV_iss KV_load")
+for j in range(16):
+    row = t[32 + j]
+    if row[0] == 0:
+        break
+    d = [row[k + 1] - row[k] for k in range(7)] + [(t[33 + j][0] - row[7]) if j < 15 and t[33 + j][0] else 0]
+    rel = [row[k] - row[0] if row[k] else 0 for k in (8, 9, 10)]
+    print(f"{j:4d} " + " ".join(f"{x:8d}" for x in d) + " | " + " ".join(f"{x:8d}" for x in rel))
