@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define BP_ABI_VERSION 1
+#define BP_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define BP_API __attribute__((visibility("default")))
@@ -74,7 +74,11 @@ enum bp_option {
                                 smem + TMA bulk stores; 0: per-thread stores */
   BP_OPT_LN_UNFUSED = 8,     /* 1: LayerNorm bwd as dx kernel + column kernels
                                 (default 0: one fused launch)                */
-  BP_OPT_LN_CTAS_PER_SM = 9  /* fused LayerNorm bwd: row blocks per SM (1..8) */
+  BP_OPT_LN_CTAS_PER_SM = 9, /* fused LayerNorm bwd: row blocks per SM (1..8) */
+  BP_OPT_LN_BWD_MODE = 10    /* bf16 LayerNorm bwd at h in {1024,2048,4096}:
+                                0 (default) two-pass fused kernel, 1 single-
+                                pass TMA-staged kernel (measured 6% slower
+                                cold in the train step, equal L2-warm)      */
 };
 BP_API int bp_set_option(int option, int value);
 
@@ -105,6 +109,10 @@ typedef struct bp_gemm_args {
   void* aux; int64_t ldaux;
   int epilogue;
   int force_simt; /* testing aid: run the SIMT kernel even for bf16 */
+  float* colsum;  /* optional (ABI 2): colsum[n] += sum_m C[m, n] over the
+                     values as stored -- the bias gradient when C is a layer's
+                     output gradient; fused into the 2-SM epilogue, else a
+                     column-reduction launch after the GEMM                 */
 } bp_gemm_args;
 BP_API int bp_gemm(const bp_gemm_args* args, void* stream);
 
@@ -156,6 +164,12 @@ BP_API int bp_attn_fwd(int dtype, int B, int S, int H, int Dh, int causal, float
 BP_API int bp_attn_bwd(int dtype, int B, int S, int H, int Dh, int causal, float scale,
                 const void* qkv, const void* o, const void* dout, const float* lse,
                 void* dqkv, float* workspace, void* stream);
+/* as bp_attn_bwd, and dbias[c] += sum_r dqkv[r, c] (fp32, the values as
+ * stored; c < 3*H*Dh) when dbias is non-NULL: the QKV bias gradient, fused
+ * into the tcgen05 kernels' epilogues (ABI 2).                           */
+BP_API int bp_attn_bwd_ex(int dtype, int B, int S, int H, int Dh, int causal, float scale,
+                   const void* qkv, const void* o, const void* dout, const float* lse,
+                   void* dqkv, float* workspace, float* dbias, void* stream);
 
 /* -------------------------------------------------------------- Adam ----
  * Fused replica-mean + AdamW on a flat parameter buffer of n elements.

@@ -21,7 +21,7 @@ bool attn_flash_supported(int dtype, int S, int Dh);
 bool attn_tc_supported(int dtype, int S, int Dh);
 int attn_tc_fwd(int B, int S, int H, int Dh, int causal, float scale, const void* qkv, void* o, float* lse,
                 cudaStream_t st);
-int attn_tc_bwd(int B, int S, int H, int Dh, int causal, float scale, const void* qkv, const void* o,
+int attn_tc_bwd(int B, int S, int H, int Dh, int causal, float scale, float* dbias, const void* qkv, const void* o,
                 const void* dout, const float* lse, void* dqkv, float* ws, cudaStream_t st);
 
 constexpr int kMaxDhPerLane = 4;  // Dh <= 128
@@ -216,15 +216,27 @@ extern "C" int bp_attn_fwd(int dtype, int B, int S, int H, int Dh, int causal, f
                          : fwd_exact<__nv_bfloat16>(B, S, H, Dh, causal, scale, qkv, o, lse, st);
 }
 
+extern "C" int bp_attn_bwd_ex(int dtype, int B, int S, int H, int Dh, int causal, float scale, const void* qkv,
+                              const void* o, const void* dout, const float* lse, void* dqkv, float* workspace,
+                              float* dbias, void* stream) {
+  if (int rc = attn_check(B, S, H, Dh)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  // tcgen05 path: the QKV bias gradient is reduced in the dK/dV and dQ
+  // kernels' epilogues; other paths take a column-reduction launch
+  if (attn_tc_supported(dtype, S, Dh))
+    return attn_tc_bwd(B, S, H, Dh, causal, scale, dbias, qkv, o, dout, lse, dqkv, workspace, st);
+  int rc;
+  if (attn_flash_supported(dtype, S, Dh))
+    rc = attn_flash_bwd(B, S, H, Dh, causal, scale, qkv, o, dout, lse, dqkv, workspace, st);
+  else
+    rc = dtype == BP_F32 ? bwd_exact<float>(B, S, H, Dh, causal, scale, qkv, o, dout, lse, dqkv, workspace, st)
+                         : bwd_exact<__nv_bfloat16>(B, S, H, Dh, causal, scale, qkv, o, dout, lse, dqkv, workspace, st);
+  if (rc || !dbias) return rc;
+  return bp_colsum_acc(dtype, B * S, 3 * H * Dh, dqkv, 3LL * H * Dh, dbias, stream);
+}
+
 extern "C" int bp_attn_bwd(int dtype, int B, int S, int H, int Dh, int causal, float scale, const void* qkv,
                            const void* o, const void* dout, const float* lse, void* dqkv, float* workspace,
                            void* stream) {
-  if (int rc = attn_check(B, S, H, Dh)) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (attn_tc_supported(dtype, S, Dh))
-    return attn_tc_bwd(B, S, H, Dh, causal, scale, qkv, o, dout, lse, dqkv, workspace, st);
-  if (attn_flash_supported(dtype, S, Dh))
-    return attn_flash_bwd(B, S, H, Dh, causal, scale, qkv, o, dout, lse, dqkv, workspace, st);
-  return dtype == BP_F32 ? bwd_exact<float>(B, S, H, Dh, causal, scale, qkv, o, dout, lse, dqkv, workspace, st)
-                         : bwd_exact<__nv_bfloat16>(B, S, H, Dh, causal, scale, qkv, o, dout, lse, dqkv, workspace, st);
+  return bp_attn_bwd_ex(dtype, B, S, H, Dh, causal, scale, qkv, o, dout, lse, dqkv, workspace, nullptr, stream);
 }

@@ -337,7 +337,7 @@ template <int Dh, bool CAUSAL>
 __global__ void __launch_bounds__(384, 1)
 dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUtensorMap map_q,
         const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse, const float* __restrict__ delta,
-        __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale, float scale_log2) {
+        __nv_bfloat16* __restrict__ dqkv, float* __restrict__ dbias, int S, int H, float scale, float scale_log2) {
   using C = Dkdv<Dh>;
   constexpr int QST = C::QST;
   extern __shared__ uint8_t smem_raw[];
@@ -541,11 +541,21 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
       tmem_ld_32x32b_x32(te + c * 32, v);
 #pragma unroll
       for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(dvrow + c * 32 + 8 * u) = pack8(v + 8 * u);
+      if (dbias) {  // V-bias gradient: column sums of this warp's 32 keys, as stored
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = bf16_round(v[i]);
+        atomicAdd(dbias + 2 * HD + h * Dh + c * 32 + lane, warp_colsum32(v, lane));
+      }
       tmem_ld_32x32b_x32(te + Dh + c * 32, v);
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] *= scale;
 #pragma unroll
       for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(dkrow + c * 32 + 8 * u) = pack8(v + 8 * u);
+      if (dbias) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = bf16_round(v[i]);
+        atomicAdd(dbias + HD + h * Dh + c * 32 + lane, warp_colsum32(v, lane));
+      }
     }
   }
   tc_fence_before();
@@ -571,7 +581,7 @@ template <int Dh, bool CAUSAL>
 __global__ void __launch_bounds__(384, 1)
 dq_tc(const __grid_constant__ CUtensorMap map_q128, const __grid_constant__ CUtensorMap map_kv64,
       const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse, const float* __restrict__ delta,
-      __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale, float scale_log2) {
+      __nv_bfloat16* __restrict__ dqkv, float* __restrict__ dbias, int S, int H, float scale, float scale_log2) {
   using C = Dq<Dh>;
   constexpr int KST = C::KST;
   extern __shared__ uint8_t smem_raw[];
@@ -736,6 +746,11 @@ dq_tc(const __grid_constant__ CUtensorMap map_q128, const __grid_constant__ CUte
       for (int i = 0; i < 32; ++i) v[i] *= scale;
 #pragma unroll
       for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(dqrow + c * 32 + 8 * u) = pack8(v + 8 * u);
+      if (dbias) {  // Q-bias gradient
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = bf16_round(v[i]);
+        atomicAdd(dbias + h * Dh + c * 32 + lane, warp_colsum32(v, lane));
+      }
     }
   }
   tc_fence_before();
@@ -743,22 +758,34 @@ dq_tc(const __grid_constant__ CUtensorMap map_q128, const __grid_constant__ CUte
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// delta[b,h,i] = <O[b,i,h,:], dO[b,i,h,:]>: Dh/8 lanes per (token, head)
+// row, one 16-byte load of O and dO per lane, rows in memory order.
 template <int Dh>
-__global__ void delta_tc_kernel(int rows_bhs, int S, int H, const __nv_bfloat16* __restrict__ o,
-                                const __nv_bfloat16* __restrict__ dout, float* __restrict__ delta) {
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (w >= rows_bhs) return;
-  const int i = w % S, h = (w / S) % H, b = w / (S * H);
-  const int64_t off = ((int64_t)b * S + i) * H * Dh + h * Dh;
+__global__ void __launch_bounds__(256) delta_tc_kernel(int rows, int S, int H, const __nv_bfloat16* __restrict__ o,
+                                                       const __nv_bfloat16* __restrict__ dout,
+                                                       float* __restrict__ delta) {
+  constexpr int LPR = Dh / 8;
+  const int gt = blockIdx.x * 256 + threadIdx.x;
+  const int row = gt / LPR, sub = gt % LPR;  // row = (b * S + i) * H + h
+  const bool ok = row < rows;
   float s = 0.f;
-  for (int d = lane * 2; d < Dh; d += 64) {
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + off + d));
-    const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dout + off + d));
-    s += a.x * c.x + a.y * c.y;
+  if (ok) {
+    const int64_t off = (int64_t)row * Dh + sub * 8;
+    const uint4 a = *reinterpret_cast<const uint4*>(o + off), c = *reinterpret_cast<const uint4*>(dout + off);
+    const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* hc = reinterpret_cast<const __nv_bfloat162*>(&c);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 fa = __bfloat1622float2(ha[j]), fc = __bfloat1622float2(hc[j]);
+      s = fmaf(fa.x, fc.x, fmaf(fa.y, fc.y, s));
+    }
   }
-  s = warp_sum(s);
-  if (lane == 0) delta[((int64_t)b * H + h) * S + i] = s;
+#pragma unroll
+  for (int m = LPR / 2; m >= 1; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+  if (ok && sub == 0) {
+    const int h = row % H, bi = row / H, i = bi % S, b = bi / S;
+    delta[((int64_t)b * H + h) * S + i] = s;
+  }
 }
 
 template <typename K>
@@ -784,11 +811,11 @@ static int fwd(int B, int S, int H, float scale, const void* qkv, void* o, float
 }
 
 template <int Dh, bool CAUSAL>
-static int bwd(int B, int S, int H, float scale, const void* qkv, const void* o, const void* dout, const float* lse,
-               void* dqkv, float* ws, cudaStream_t st) {
+static int bwd(int B, int S, int H, float scale, float* dbias, const void* qkv, const void* o, const void* dout,
+               const float* lse, void* dqkv, float* ws, cudaStream_t st) {
   float* delta = ws;
   const int rows = B * H * S;
-  delta_tc_kernel<Dh><<<(rows + 7) / 8, 256, 0, st>>>(rows, S, H, (const __nv_bfloat16*)o,
+  delta_tc_kernel<Dh><<<(int)(((int64_t)rows * (Dh / 8) + 255) / 256), 256, 0, st>>>(rows, S, H, (const __nv_bfloat16*)o,
                                                        (const __nv_bfloat16*)dout, delta);
   count_launch();
   CUtensorMap kv128, q64, do64, q128, kv64, do128;
@@ -808,10 +835,10 @@ static int bwd(int B, int S, int H, float scale, const void* qkv, const void* o,
     once = true;
   }
   const float sl2 = scale * kLog2e;
-  k1<<<dim3(B * H, S / 128), 384, Dkdv<Dh>::SMEM, st>>>(kv128, q64, do64, lse, delta, (__nv_bfloat16*)dqkv, S, H,
+  k1<<<dim3(B * H, S / 128), 384, Dkdv<Dh>::SMEM, st>>>(kv128, q64, do64, lse, delta, (__nv_bfloat16*)dqkv, dbias, S, H,
                                                          scale, sl2);
   count_launch();
-  k2<<<dim3(B * H, S / 128), 384, Dq<Dh>::SMEM, st>>>(q128, kv64, do128, lse, delta, (__nv_bfloat16*)dqkv, S, H,
+  k2<<<dim3(B * H, S / 128), 384, Dq<Dh>::SMEM, st>>>(q128, kv64, do128, lse, delta, (__nv_bfloat16*)dqkv, dbias, S, H,
                                                        scale, sl2);
   count_launch();
   BP_CHECK_LAUNCH("attn_bwd_tc");
@@ -843,13 +870,13 @@ int attn_tc_fwd(int B, int S, int H, int Dh, int causal, float scale, const void
                 : fat::fwd<64, false>(B, S, H, scale, qkv, o, lse, st);
 }
 
-int attn_tc_bwd(int B, int S, int H, int Dh, int causal, float scale, const void* qkv, const void* o,
+int attn_tc_bwd(int B, int S, int H, int Dh, int causal, float scale, float* dbias, const void* qkv, const void* o,
                 const void* dout, const float* lse, void* dqkv, float* ws, cudaStream_t st) {
   if (Dh == 128)
-    return causal ? fat::bwd<128, true>(B, S, H, scale, qkv, o, dout, lse, dqkv, ws, st)
-                  : fat::bwd<128, false>(B, S, H, scale, qkv, o, dout, lse, dqkv, ws, st);
-  return causal ? fat::bwd<64, true>(B, S, H, scale, qkv, o, dout, lse, dqkv, ws, st)
-                : fat::bwd<64, false>(B, S, H, scale, qkv, o, dout, lse, dqkv, ws, st);
+    return causal ? fat::bwd<128, true>(B, S, H, scale, dbias, qkv, o, dout, lse, dqkv, ws, st)
+                  : fat::bwd<128, false>(B, S, H, scale, dbias, qkv, o, dout, lse, dqkv, ws, st);
+  return causal ? fat::bwd<64, true>(B, S, H, scale, dbias, qkv, o, dout, lse, dqkv, ws, st)
+                : fat::bwd<64, false>(B, S, H, scale, dbias, qkv, o, dout, lse, dqkv, ws, st);
 }
 
 }  // namespace bp

@@ -109,6 +109,16 @@ BP_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// 1-D bulk copy global -> shared (16-byte aligned, bytes % 16 == 0),
+// completion counted on `bar` (expect_tx issued by the caller).
+BP_DEV void bulk_g2s(void* smem_dst, const void* g, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(g), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // 2-D TMA tile load global -> shared, completion signalled on `bar`.
 BP_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
@@ -322,6 +332,24 @@ BP_DEV void tmem_ld_32x32b_x32_pair(uint32_t taddr0, uint32_t taddr1, float (&a)
 BP_DEV void named_bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
+
+// Column sums of a 32 x 32 tile held one row per lane (v[j] = row lane,
+// column j): a reduce-scatter butterfly (31 shuffles); afterwards lane l
+// returns the sum over the warp's 32 rows of column l.  Destroys v.
+BP_DEV float warp_colsum32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int stage = 16; stage >= 1; stage >>= 1) {
+    const bool up = (lane & stage) != 0;
+#pragma unroll
+    for (int i = 0; i < stage; ++i) {
+      const float send = up ? v[i] : v[i + stage];
+      const float keep = up ? v[i + stage] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, stage);
+    }
+  }
+  return v[0];
+}
+BP_DEV float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
 // UMMA shared-memory descriptor, SWIZZLE_128B, sm_100 version field = 1.
 //   K-major tile : rows of 128 B (64 bf16 along K), 8-row atoms 1024 B apart

@@ -42,11 +42,12 @@ __global__ void __launch_bounds__(256) colred_kernel(int rows, int cols, int row
     }
   };
   if (c0 < cols) {
-    // 4 independent rows (8 apart) per iteration keep 4 loads in flight
-    for (int rb = r0 + ty; rb < r1; rb += 32) {
-      float v[4][8], w[4][8];
+    // UR independent rows (8 apart) per iteration keep UR loads in flight
+    constexpr int UR = 4;
+    for (int rb = r0 + ty; rb < r1; rb += 8 * UR) {
+      float v[UR][8], w[UR][8];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < UR; ++k) {
         const int r = rb + 8 * k;
         if (r < r1) {
           load8(a + (int64_t)r * lda + c0, v[k]);
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(256) colred_kernel(int rows, int cols, int row
         }
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < UR; ++k) {
         const int r = rb + 8 * k;
         if (r >= r1) continue;
         if (MODE == 0) {

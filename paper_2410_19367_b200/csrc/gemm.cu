@@ -38,6 +38,7 @@ struct Epi {
   int vec_ok;
   int nostore;  // debug: drain TMEM but skip the global epilogue (BP_OPT_GEMM_DEBUG)
   int tma_store;  // 2-SM kernel: stage 32-column chunks in smem, TMA-store them
+  float* colsum;  // optional: colsum[n] += sum over rows of C as stored (TMA epilogue only)
 };
 
 BP_DEV float ld_any(const void* p, int dtype, int64_t i) {
@@ -346,6 +347,13 @@ BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap
       }
     }
     stage_row32(unit, lane, ep.c_dtype, v);
+    if (ep.colsum) {  // bias gradient: column sums of this warp's 32 rows, as stored
+      float t[32];
+      const bool row_ok = row0 + lane < ep.M;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) t[i] = row_ok ? (ep.c_dtype == BP_BF16 ? bf16_round(v[i]) : v[i]) : 0.f;
+      atomicAdd(ep.colsum + c0 + lane, warp_colsum32(t, lane));
+    }
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
@@ -1117,6 +1125,18 @@ static int dispatch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+template <typename T, int MODE>
+int launch_colred(int rows, int cols, const void* a, int64_t lda, const void* x, const float* mean, const float* rstd,
+                  float* out0, float* out1, cudaStream_t st);
+
+// Unfused bias gradient: a column-reduction launch over C after the GEMM.
+static int gemm_colsum_after(const bp_gemm_args& g, cudaStream_t st) {
+  if (!g.colsum) return BP_OK;
+  return g.c_dtype == BP_F32
+             ? launch_colred<float, 0>(g.M, g.N, g.C, g.ldc, nullptr, nullptr, nullptr, g.colsum, nullptr, st)
+             : launch_colred<__nv_bfloat16, 0>(g.M, g.N, g.C, g.ldc, nullptr, nullptr, nullptr, g.colsum, nullptr, st);
+}
+
 }  // namespace bp
 
 using namespace bp;
@@ -1146,6 +1166,7 @@ extern "C" int bp_gemm(const bp_gemm_args* gp, void* stream) {
   ep.residual = g.residual; ep.ldr = g.ldr; ep.aux = g.aux; ep.ldaux = g.ldaux; ep.epilogue = g.epilogue;
   ep.nostore = gemm_debug_nostore();
   ep.tma_store = 0;
+  ep.colsum = nullptr;
   const int esz = g.c_dtype == BP_F32 ? 4 : 2;
   ep.vec_ok = aligned16(g.C) && (g.ldc * esz) % 16 == 0 && (!g.bias || aligned16(g.bias)) &&
               (!g.residual || (aligned16(g.residual) && (g.ldr * esz) % 16 == 0)) &&
@@ -1164,11 +1185,16 @@ extern "C" int bp_gemm(const bp_gemm_args* gp, void* stream) {
                      ((!g.residual && g.epilogue != BP_EPI_DGELU) || g.c_dtype == BP_BF16) &&
                      !(g.residual && (ep.accumulate || g.epilogue != BP_EPI_NONE)) &&
                      !(ep.accumulate && g.epilogue != BP_EPI_NONE);
-      return dispatch_tc2(g, ep, st);
+      if (g.colsum && ep.tma_store && !ep.accumulate) {
+        ep.colsum = g.colsum;
+        return dispatch_tc2(g, ep, st);
+      }
+      if (int rc = dispatch_tc2(g, ep, st)) return rc;
+      return gemm_colsum_after(g, st);
     }
     const int tiles256 = ((g.M + 127) / 128) * ((g.N + 255) / 256);
-    if (g.N > 128 && tiles256 >= num_sms()) return dispatch_tc<256>(g, ep, st);
-    return dispatch_tc<128>(g, ep, st);
+    const int rc = (g.N > 128 && tiles256 >= num_sms()) ? dispatch_tc<256>(g, ep, st) : dispatch_tc<128>(g, ep, st);
+    return rc ? rc : gemm_colsum_after(g, st);
   }
   dim3 grid((g.N + 63) / 64, (g.M + 63) / 64);
   if (g.in_dtype == BP_F32)
@@ -1180,5 +1206,5 @@ extern "C" int bp_gemm(const bp_gemm_args* gp, void* stream) {
         static_cast<const __nv_bfloat16*>(g.B), g.ldb, g.b_kmajor, ep);
   count_launch();
   BP_CHECK_LAUNCH("gemm_simt");
-  return BP_OK;
+  return gemm_colsum_after(g, st);
 }

@@ -13,6 +13,7 @@ void count_launch();
 int num_sms();
 bool ln_bwd_unfused();
 int ln_ctas_per_sm();
+int ln_bwd_mode();
 template <typename T, int MODE>
 int launch_colred(int rows, int cols, const void* a, int64_t lda, const void* x, const float* mean, const float* rstd,
                   float* out0, float* out1, cudaStream_t st);
@@ -309,6 +310,163 @@ __global__ void __launch_bounds__(32 * NV * RG) ln_bwd_fused(int rows, int rows_
   }
 }
 
+// Single-pass bf16 backward.  One CTA per SM owns a contiguous block of
+// rows; thread 0 brings the block's x, dy and dres rows into shared memory
+// with three 1-D bulk (TMA) copies issued at once, so the whole block is in
+// flight from the first cycle.  Thread t then owns the 16-byte column vector
+// t of every row: the two per-row dot products of all rows are reduced in one
+// multi-value warp butterfly (31 shuffles for up to 16 rows) plus one
+// cross-warp pass, dx is written straight from registers, and the dgamma /
+// dbeta / dx column sums stay in registers and leave as one 16-byte vector
+// reduction per 4 columns.  HBM traffic = read dy, x, dres + write dx.
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) ln_bwd_tma(int rows, int rows_per, int rmax,
+                                                   const __nv_bfloat16* __restrict__ dy,
+                                                   const __nv_bfloat16* __restrict__ x,
+                                                   const __nv_bfloat16* __restrict__ g,
+                                                   const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                   const __nv_bfloat16* __restrict__ dres,
+                                                   __nv_bfloat16* __restrict__ dx, float* __restrict__ dgamma,
+                                                   float* __restrict__ dbeta, float* __restrict__ dxsum) {
+  using V = Vec<__nv_bfloat16>;
+  using U = uint4;
+  constexpr int cols = NT * 8, NW = NT / 32;
+  extern __shared__ __align__(128) uint8_t ln_smem[];  // [3][rmax][cols] bf16: x, dy, dres
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ float red[NW][32];
+  __shared__ float fin[32];
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int r0 = blockIdx.x * rows_per, r1 = min(rows, r0 + rows_per);
+  if (r0 >= r1) return;
+  const U* SX = reinterpret_cast<const U*>(ln_smem);
+  const U* SD = SX + (size_t)rmax * NT;
+  const U* SR = SD + (size_t)rmax * NT;
+  U* DX = reinterpret_cast<U*>(dx);
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  float gg[8];
+  V::unpack(reinterpret_cast<const U*>(g)[t], gg);
+  float sg[8] = {}, sb[8] = {}, sx[8] = {};
+  uint32_t phase = 0;
+  for (int rb = r0; rb < r1; rb += rmax) {
+    const int nr = min(rmax, r1 - rb);
+    if (t == 0) {
+      if (rb != r0) fence_proxy_async_smem();  // generic reads of the last batch before async overwrite
+      const uint32_t bytes = (uint32_t)nr * cols * 2;
+      mbar_expect_tx(&bar, (dres ? 3u : 2u) * bytes);
+      bulk_g2s((void*)SX, x + (int64_t)rb * cols, bytes, &bar);
+      bulk_g2s((void*)SD, dy + (int64_t)rb * cols, bytes, &bar);
+      if (dres) bulk_g2s((void*)SR, dres + (int64_t)rb * cols, bytes, &bar);
+    }
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    float mu[16], rs[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      mu[k] = k < nr ? mean[rb + k] : 0.f;
+      rs[k] = k < nr ? rstd[rb + k] : 0.f;
+    }
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      if (k < nr) {
+        float a[8], d[8];
+        V::unpack(SX[k * NT + t], a);
+        V::unpack(SD[k * NT + t], d);
+        float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float dh = d[j] * gg[j];
+          s1 += dh;
+          s2 += dh * (a[j] - mu[k]);
+        }
+        v[2 * k] = s1;
+        v[2 * k + 1] = s2 * rs[k];
+      }
+    }
+    // butterfly reduce-scatter: afterwards lane l holds the warp sum of value l
+#pragma unroll
+    for (int stage = 16; stage >= 1; stage >>= 1) {
+      const bool up = (lane & stage) != 0;
+#pragma unroll
+      for (int i = 0; i < stage; ++i) {
+        const float send = up ? v[i] : v[i + stage];
+        const float keep = up ? v[i + stage] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, stage);
+      }
+    }
+    red[warp][lane] = v[0];
+    __syncthreads();
+    if (t < 32) {
+      float a = 0.f;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) a += red[w][t];
+      fin[t] = a * (1.f / cols);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      if (k < nr) {
+        const float s1 = fin[2 * k], s2 = fin[2 * k + 1];
+        float a[8], d[8], rr[8], o[8];
+        V::unpack(SX[k * NT + t], a);
+        V::unpack(SD[k * NT + t], d);
+        if (dres) V::unpack(SR[k * NT + t], rr);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float xh = (a[j] - mu[k]) * rs[k];
+          o[j] = rs[k] * (d[j] * gg[j] - s1 - xh * s2) + (dres ? rr[j] : 0.f);
+          sg[j] += d[j] * xh;
+          sb[j] += d[j];
+        }
+        const U packed = V::pack(o);
+        DX[(int64_t)(rb + k) * NT + t] = packed;
+        if (dxsum) {
+          V::unpack(packed, o);  // as stored
+#pragma unroll
+          for (int j = 0; j < 8; ++j) sx[j] += o[j];
+        }
+      }
+    }
+    __syncthreads();  // shared rows / red / fin are reused by the next row batch
+  }
+#pragma unroll
+  for (int j = 0; j < 8; j += 4) {
+    const int c = t * 8 + j;
+    if (dgamma) red_add_v4(dgamma + c, sg[j], sg[j + 1], sg[j + 2], sg[j + 3]);
+    if (dbeta) red_add_v4(dbeta + c, sb[j], sb[j + 1], sb[j + 2], sb[j + 3]);
+    if (dxsum) red_add_v4(dxsum + c, sx[j], sx[j + 1], sx[j + 2], sx[j + 3]);
+  }
+}
+
+template <int NT>
+static int launch_ln_bwd_tma(int rows, const void* dy, const void* x, const void* g, const float* mean,
+                             const float* rstd, const void* dres, void* dx, float* dgamma, float* dbeta, float* dxsum,
+                             cudaStream_t st) {
+  constexpr int cols = NT * 8;
+  int rmax = 196608 / (6 * cols);
+  if (rmax > 16) rmax = 16;
+  const int rows_per = (rows + num_sms() - 1) / num_sms();
+  const int grid = (rows + rows_per - 1) / rows_per;
+  const size_t smem = (size_t)3 * rmax * cols * 2;
+  static bool attr = false;
+  if (!attr) {
+    BP_CUDA(cudaFuncSetAttribute(ln_bwd_tma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  ln_bwd_tma<NT><<<grid, NT, smem, st>>>(rows, rows_per, rmax, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
+                                         (const __nv_bfloat16*)g, mean, rstd, (const __nv_bfloat16*)dres,
+                                         (__nv_bfloat16*)dx, dgamma, dbeta, dxsum);
+  count_launch();
+  BP_CHECK_LAUNCH("ln_bwd_tma");
+  return BP_OK;
+}
+
 // ---------------------------------------------------------- generic path --
 template <typename T>
 __global__ void ln_fwd_generic(int cols, const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b,
@@ -443,6 +601,14 @@ static int ln_bwd_t(int rows, int cols, const void* dy, const void* x, const voi
                     reinterpret_cast<uintptr_t>(dres) | reinterpret_cast<uintptr_t>(dx) |
                     reinterpret_cast<uintptr_t>(dgamma) | reinterpret_cast<uintptr_t>(dbeta) |
                     reinterpret_cast<uintptr_t>(dxsum)) & 15) == 0;
+  if (sizeof(T) == 2 && al && !ln_bwd_unfused() && ln_bwd_mode() == 1) {
+    switch (cols) {
+      case 1024: return launch_ln_bwd_tma<128>(rows, dy, x, g, mean, rstd, dres, dx, dgamma, dbeta, dxsum, st);
+      case 2048: return launch_ln_bwd_tma<256>(rows, dy, x, g, mean, rstd, dres, dx, dgamma, dbeta, dxsum, st);
+      case 4096: return launch_ln_bwd_tma<512>(rows, dy, x, g, mean, rstd, dres, dx, dgamma, dbeta, dxsum, st);
+      default: break;
+    }
+  }
   const int nvf = cols % (32 * E) == 0 ? cols / (32 * E) : 0;
   if (al && (nvf == 1 || nvf == 2 || nvf == 4 || nvf == 8 || nvf == 16) && !ln_bwd_unfused()) {
     // one CTA of rows per SM; fewer CTAs = fewer column reductions at the end

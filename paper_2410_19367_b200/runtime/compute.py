@@ -12,10 +12,11 @@ Per half-block (x = residual stream, M = B*S tokens):
              (bias + residual fused in the GEMM epilogue)
   mlp  fwd : m=LN2(x) | g=gelu(m W1^T+b1), u saved (GELU epilogue) |
              x'=x+g W2^T+b2
-  attn bwd : dWo+=dy^T o | dbo+=sum dy | do=dy Wo | dqkv=attn_bwd |
-             dWqkv+=dqkv^T a | dbqkv | da=dqkv Wqkv | dx=dy+LN1'(da)
-  mlp  bwd : dW2+=dy^T g | db2 | du=(dy W2)*gelu'(u) (dGELU epilogue) |
-             dW1+=du^T m | db1 | dm=du W1 | dx=dy+LN2'(dm)
+  attn bwd : dWo+=dy^T o | dbo+=sum dy | do=dy Wo | dqkv=attn_bwd (+dbqkv
+             in its epilogues) | dWqkv+=dqkv^T a | da=dqkv Wqkv |
+             dx=dy+LN1'(da)
+  mlp  bwd : dW2+=dy^T g | db2 | du=(dy W2)*gelu'(u) (dGELU epilogue, +db1
+             column sums) | dW1+=du^T m | dm=du W1 | dx=dy+LN2'(dm)
   head     : xf=LNf(x) | logits=xf Wlm^T | fused softmax-CE fwd+bwd in place
              (loss to the micro-batch's slot) ; bwd: dxf=dlogits Wlm,
              dWlm+=dlogits^T xf, dx=LNf'(dxf)
@@ -158,10 +159,11 @@ class StageCompute:
                 do = pool.get((M, h), dt, stream)
                 ops.gemm(dy, P[p + "attn.proj.w"], do, b_kmajor=False, stream=stream)
                 dqkv = pool.get((M, 3 * h), dt, stream)
+                # the QKV bias gradient (column sums of dqkv) comes out of the
+                # attention backward's epilogues
                 ops.attn_bwd(qkv, o, do, lse, dqkv, ws, cfg.micro_batch, cfg.seq, H, Dh, cfg.causal, scale,
-                             stream=stream)
+                             stream=stream, dbias=G[p + "attn.qkv.b"])
                 ops.gemm(dqkv, a, G[p + "attn.qkv.w"], a_kmajor=False, b_kmajor=False, beta=1.0, stream=stream)
-                ops.colsum_acc(dqkv, G[p + "attn.qkv.b"], stream=stream)
                 da = pool.get((M, h), dt, stream)
                 ops.gemm(dqkv, P[p + "attn.qkv.w"], da, b_kmajor=False, stream=stream)
                 ops.layernorm_bwd(da, x, P[p + "ln1.w"], mean, rstd, dx, G[p + "ln1.w"], G[p + "ln1.b"], dres=dy,
@@ -173,9 +175,11 @@ class StageCompute:
                 if not bias_done:
                     ops.colsum_acc(dy, G[p + "mlp.fc2.b"], stream=stream)
                 du = pool.get((M, cfg.ffn), dt, stream)
-                ops.gemm(dy, P[p + "mlp.fc2.w"], du, b_kmajor=False, aux=u, epilogue=EPI_DGELU, stream=stream)
+                # du = (dy W2) * gelu'(u); its column sums (the fc1 bias
+                # gradient) are reduced in the same GEMM epilogue
+                ops.gemm(dy, P[p + "mlp.fc2.w"], du, b_kmajor=False, aux=u, epilogue=EPI_DGELU, stream=stream,
+                         colsum=G[p + "mlp.fc1.b"])
                 ops.gemm(du, m, G[p + "mlp.fc1.w"], a_kmajor=False, b_kmajor=False, beta=1.0, stream=stream)
-                ops.colsum_acc(du, G[p + "mlp.fc1.b"], stream=stream)
                 dm = pool.get((M, h), dt, stream)
                 ops.gemm(du, P[p + "mlp.fc1.w"], dm, b_kmajor=False, stream=stream)
                 ops.layernorm_bwd(dm, x, P[p + "ln2.w"], mean, rstd, dx, G[p + "ln2.w"], G[p + "ln2.b"], dres=dy,

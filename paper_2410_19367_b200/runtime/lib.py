@@ -12,15 +12,16 @@ import threading
 
 __all__ = ["lib", "GemmArgs", "check", "LIB_PATH", "BP_F32", "BP_BF16", "EPI_NONE", "EPI_GELU", "EPI_DGELU",
            "OPT_ATTN_EXACT", "OPT_GEMM_SIMT", "OPT_GEMM_MODE",
-           "OPT_STREAM_K", "OPT_GEMM_WIDE", "OPT_GEMM_DEBUG", "OPT_GEMM_TMA_STORE", "OPT_LN_UNFUSED"]
+           "OPT_STREAM_K", "OPT_GEMM_WIDE", "OPT_GEMM_DEBUG", "OPT_GEMM_TMA_STORE", "OPT_LN_UNFUSED",
+           "OPT_LN_BWD_MODE"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "libbitpipe_b200.so")
 
 BP_F32, BP_BF16 = 0, 1
 EPI_NONE, EPI_GELU, EPI_DGELU = 0, 1, 2
 OPT_ATTN_EXACT, OPT_GEMM_SIMT, OPT_GEMM_MODE, OPT_STREAM_K, OPT_GEMM_WIDE = 1, 2, 3, 4, 5
-OPT_GEMM_DEBUG, OPT_GEMM_TMA_STORE, OPT_LN_UNFUSED = 6, 7, 8
-ABI_VERSION = 1
+OPT_GEMM_DEBUG, OPT_GEMM_TMA_STORE, OPT_LN_UNFUSED, OPT_LN_BWD_MODE = 6, 7, 8, 10
+ABI_VERSION = 2
 
 _vp = ctypes.c_void_p
 _i32, _i64, _f32 = ctypes.c_int, ctypes.c_int64, ctypes.c_float
@@ -35,7 +36,7 @@ class GemmArgs(ctypes.Structure):
         ("alpha", _f32), ("beta", _f32),
         ("bias", _vp), ("residual", _vp), ("ldr", _i64),
         ("aux", _vp), ("ldaux", _i64),
-        ("epilogue", _i32), ("force_simt", _i32),
+        ("epilogue", _i32), ("force_simt", _i32), ("colsum", _vp),
     ]
 
 
@@ -58,6 +59,7 @@ _SIGS = {
     "bp_attn_workspace_bytes": (_i64, [_i32, _i32, _i32, _i32]),
     "bp_attn_fwd": (_i32, [_i32, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _vp, _vp, _vp]),
     "bp_attn_bwd": (_i32, [_i32, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "bp_attn_bwd_ex": (_i32, [_i32, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "bp_adam": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _f32, _f32, _f32, _f32, _i32, _f32,
                        _vp]),
 }

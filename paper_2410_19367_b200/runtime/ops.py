@@ -69,8 +69,9 @@ def launch_count() -> int:
 
 
 def gemm(a, b, c, *, a_kmajor=True, b_kmajor=True, alpha=1.0, beta=0.0, bias=None, residual=None, aux=None,
-         epilogue=EPI_NONE, stream=None, force_simt=False):
-    """c = epilogue(alpha * op(a) @ op(b)); see include/bitpipe.h for op()."""
+         epilogue=EPI_NONE, stream=None, force_simt=False, colsum=None):
+    """c = epilogue(alpha * op(a) @ op(b)); see include/bitpipe.h for op().
+    colsum (fp32 [N]): += column sums of c as stored (fused bias gradient)."""
     for t, n in ((a, "a"), (b, "b"), (c, "c")):
         _rowmajor(t, n)
     M, K = (a.shape if a_kmajor else (a.shape[1], a.shape[0]))
@@ -96,6 +97,10 @@ def gemm(a, b, c, *, a_kmajor=True, b_kmajor=True, alpha=1.0, beta=0.0, bias=Non
         g.aux, g.ldaux = aux.data_ptr(), aux.stride(0)
     g.epilogue = int(epilogue)
     g.force_simt = int(bool(force_simt))
+    if colsum is not None:
+        if colsum.dtype != torch.float32 or colsum.numel() != N:
+            raise ValueError("colsum must be an fp32 [N] tensor")
+        g.colsum = colsum.data_ptr()
     probe = _gemm_probe is not None and g.in_dtype == BP_BF16
     if probe:
         st = stream if stream is not None else torch.cuda.current_stream()
@@ -157,9 +162,13 @@ def attn_fwd(qkv, o, lse, B, S, H, Dh, causal, scale, stream=None):
                             _s(stream)), "bp_attn_fwd")
 
 
-def attn_bwd(qkv, o, dout, lse, dqkv, workspace, B, S, H, Dh, causal, scale, stream=None):
-    check(lib().bp_attn_bwd(_dt(qkv), B, S, H, Dh, int(bool(causal)), float(scale), _p(qkv), _p(o), _p(dout),
-                            _p(lse), _p(dqkv), _p(workspace), _s(stream)), "bp_attn_bwd")
+def attn_bwd(qkv, o, dout, lse, dqkv, workspace, B, S, H, Dh, causal, scale, stream=None, dbias=None):
+    """dqkv = attention backward; dbias (fp32 [3*H*Dh]) += column sums of dqkv
+    (the QKV bias gradient, fused into the tcgen05 kernels)."""
+    if dbias is not None and (dbias.dtype != torch.float32 or dbias.numel() != 3 * H * Dh):
+        raise ValueError("dbias must be an fp32 [3*H*Dh] tensor")
+    check(lib().bp_attn_bwd_ex(_dt(qkv), B, S, H, Dh, int(bool(causal)), float(scale), _p(qkv), _p(o), _p(dout),
+                               _p(lse), _p(dqkv), _p(workspace), _p(dbias), _s(stream)), "bp_attn_bwd")
 
 
 def adam(master, grad_a, grad_b, m, v, param_a, param_b, *, lr, beta1, beta2, eps, weight_decay, step,

@@ -78,13 +78,20 @@ def test_gemm_epilogues(M, N, K, gemm_mode):
     pre = acc + b.float()
     assert _relerr(aux.float(), pre) < 1e-2
     assert _relerr(G.float(), _gelu(aux.float())) < 1e-2
-    # dgelu
+    # dgelu, with the fused bias-gradient column sums of the output
     D = torch.empty_like(C)
-    ops.gemm(X, W, D, aux=aux, epilogue=EPI_DGELU)
+    cs = torch.full((N,), 0.25, device=dev)
+    ops.gemm(X, W, D, aux=aux, epilogue=EPI_DGELU, colsum=cs)
     x = aux.float().requires_grad_(True)
     _gelu(x).backward(torch.ones_like(x))
     assert _relerr(D.float(), acc * x.grad) < 1e-2
     torch.cuda.synchronize()
+    assert _relerr(cs, 0.25 + D.float().sum(0)) < 1e-5
+    # column sums of a plain bf16 output too
+    cs2 = torch.zeros(N, device=dev)
+    ops.gemm(X, W, C, colsum=cs2)
+    torch.cuda.synchronize()
+    assert _relerr(cs2, C.float().sum(0)) < 1e-5
 
 
 @pytest.mark.parametrize("M,N,K,ak,bk", [(512, 768, 256, True, True), (300, 416, 128, True, True),
@@ -157,11 +164,14 @@ def test_gemm_tc_matches_simt_bitwise_close():
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("rows,cols", [(64, 64), (300, 1024), (2048, 2048), (17, 100), (5, 256), (2048, 4096)])
-@pytest.mark.parametrize("unfused", [0, 1], ids=["fused", "unfused"])
-def test_layernorm_bwd_colsum(dtype, rows, cols, unfused):
+@pytest.mark.parametrize("path", ["tma", "twopass", "unfused"])
+def test_layernorm_bwd_colsum(dtype, rows, cols, path):
     """LayerNorm backward with the fused dx column sum (bias grad of the
-    previous half-block), fused and split-kernel paths, vs torch fp32."""
-    from paper_2410_19367_b200.runtime.lib import OPT_LN_UNFUSED
+    previous half-block): single-pass TMA-staged kernel (bf16, h in
+    {1024,2048,4096}), two-pass fused kernel and split-kernel paths, vs torch
+    fp32."""
+    from paper_2410_19367_b200.runtime.lib import OPT_LN_BWD_MODE, OPT_LN_UNFUSED
+    unfused = int(path == "unfused")
     x = torch.randn(rows, cols, device="cuda").to(dtype)
     g = (1 + 0.1 * torch.randn(cols, device="cuda")).to(dtype)
     b = (0.1 * torch.randn(cols, device="cuda")).to(dtype)
@@ -181,11 +191,13 @@ def test_layernorm_bwd_colsum(dtype, rows, cols, unfused):
     db = torch.full((cols,), -0.5, device="cuda")
     cs = torch.ones(cols, device="cuda")
     ops.set_option(OPT_LN_UNFUSED, unfused)
+    ops.set_option(OPT_LN_BWD_MODE, int(path == "tma"))
     try:
         ops.layernorm_bwd(dy, x, g, mean, rstd, dx, dg, db, dres=dres, dx_colsum=cs)
         torch.cuda.synchronize()
     finally:
         ops.set_option(OPT_LN_UNFUSED, 0)
+        ops.set_option(OPT_LN_BWD_MODE, 0)
     tol = 1e-5 if dtype == torch.float32 else 2e-2
     assert _relerr(dx.float(), xr.grad + dres.float()) < tol
     assert _relerr(dg, 0.5 + gr.grad) < tol
@@ -288,9 +300,12 @@ def test_attention(dtype, B, S, H, Dh, causal):
     oref.backward(dout.float())
     dqkv = torch.empty_like(qkv)
     ws = torch.empty(ops.attn_workspace_numel(B, S, H, Dh), device="cuda")
-    ops.attn_bwd(qkv, o, dout, lse, dqkv, ws, B, S, H, Dh, causal, scale)
+    dbias = torch.ones(3 * H * Dh, device="cuda")
+    ops.attn_bwd(qkv, o, dout, lse, dqkv, ws, B, S, H, Dh, causal, scale, dbias=dbias)
     torch.cuda.synchronize()
     assert _relerr(dqkv.float(), x.grad) < (1e-4 if dtype == torch.float32 else 3e-2)
+    # fused QKV bias gradient = 1 + column sums of dqkv as stored
+    assert _relerr(dbias, 1 + dqkv.float().sum(0)) < 1e-5
 
 
 def test_adam_matches_torch():

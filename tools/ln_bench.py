@@ -4,7 +4,7 @@ import sys
 import torch
 sys.path.insert(0, ".")
 from paper_2410_19367_b200.runtime import ops
-from paper_2410_19367_b200.runtime.lib import OPT_LN_UNFUSED
+from paper_2410_19367_b200.runtime.lib import OPT_LN_BWD_MODE, OPT_LN_UNFUSED
 
 
 def timeit(fn, iters=20):
@@ -45,6 +45,9 @@ for cols in (2048, 4096):
     t_copy = timeit(lambda: y.copy_(x))
     t_fwd = timeit(lambda: ops.layernorm_fwd(x, g, b, y, mean, rstd))
     ops.set_option(OPT_LN_UNFUSED, 0)
+    ops.set_option(OPT_LN_BWD_MODE, 1)
+    t_tma = timeit(lambda: ops.layernorm_bwd(dy, x, g, mean, rstd, dx, dg, db, dres=dres, dx_colsum=cs))
+    ops.set_option(OPT_LN_BWD_MODE, 0)
     t_bf = timeit(lambda: ops.layernorm_bwd(dy, x, g, mean, rstd, dx, dg, db, dres=dres, dx_colsum=cs))
     t_bf0 = timeit(lambda: ops.layernorm_bwd(dy, x, g, mean, rstd, dx, dg, db, dres=dres))
     ops.set_option(OPT_LN_UNFUSED, 1)
@@ -58,6 +61,10 @@ for cols in (2048, 4096):
     ops.set_option(9, 1)
     print("fused ln_bwd by CTAs/SM 1..4:", " ".join(f"{t:.1f}" for t in cps))
     t_cs = timeit(lambda: ops.colsum_acc(dy, cs))
+    wide = torch.randn(rows, 4 * cols, device="cuda").bfloat16()
+    cs4 = torch.zeros(4 * cols, device="cuda")
+    t_cs4 = timeit(lambda: ops.colsum_acc(wide, cs4))
+    print(f"ln_bwd single-pass TMA {t_tma:.1f} us vs two-pass {t_bf:.1f} us; colsum {rows}x{4*cols} {t_cs4:.1f} us")
     print(f"{rows}x{cols} ({MB:.0f} MB/matrix): copy {t_copy:.1f} us ({2*MB/t_copy:.2f} TB/s) | ln_fwd {t_fwd:.1f} | "
           f"ln_bwd fused {t_bf:.1f} (no colsum {t_bf0:.1f}) | unfused {t_bu:.1f} (no colsum {t_bu0:.1f}) | "
           f"colsum {t_cs:.1f} us", flush=True)
