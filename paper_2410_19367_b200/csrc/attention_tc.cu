@@ -314,17 +314,18 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
 // CTA = 128 keys, 384 threads.  Two compute warpgroups ping-pong over the
 // 64-query tiles (warps 4-7 take even tiles, warps 8-11 odd ones), so one
 // group's exp / dS math overlaps the other's and the tensor pipe always has
-// the next S^T / dP^T pair queued: S^T / dP^T are double-buffered in TMEM and
-// P^T / dS^T in shared memory.  Q / dO / LSE / delta stream through a
-// QST-deep TMA ring.
+// the next S^T / dP^T pair queued (double-buffered in TMEM).  P^T and dS^T
+// are written back as bf16 into the TMEM columns their S^T / dP^T came from
+// and feed dV += P^T dO and dK += dS^T Q as tensor-memory A operands, so the
+// shared-memory port (the bound of this kernel) only serves the Q / dO / K /
+// V operand reads.  Q / dO / LSE / delta stream through a QST-deep TMA ring.
 template <int Dh>
 struct Dkdv {
   static constexpr int DC = Dh / 64;
-  static constexpr int QST = 3;
+  static constexpr int QST = 4;
   static constexpr uint32_t KT = 128 * Dh * 2;  // K / V tile (128 keys)
   static constexpr uint32_t QT = 64 * Dh * 2;   // Q / dO tile (64 queries)
-  static constexpr uint32_t PB = 128 * 64 * 2;  // P^T / dS^T tile
-  static constexpr size_t SMEM = 1024 + 2 * KT + QST * 2 * QT + 4 * PB + QST * 512 + 512;
+  static constexpr size_t SMEM = 1024 + 2 * KT + QST * 2 * QT + QST * 512 + 512;
 };
 
 BP_DEV float4 lds4(uint32_t addr) {
@@ -344,20 +345,19 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = smem;
   uint8_t* sV = smem + C::KT;
-  uint8_t* sQ0 = smem + 2 * C::KT;     // stage s: Q at sQ0 + 2 s QT, dO right after
-  uint8_t* sPD = sQ0 + QST * 2 * C::QT;  // buffer g: P^T at sPD + 2 g PB, dS^T right after
-  float* sL0 = reinterpret_cast<float*>(sPD + 4 * C::PB);  // stage s: 64 lse then 64 delta
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sPD + 4 * C::PB + QST * 512);
+  uint8_t* sQ0 = smem + 2 * C::KT;  // stage s: Q at sQ0 + 2 s QT, dO right after
+  float* sL0 = reinterpret_cast<float*>(sQ0 + QST * 2 * C::QT);  // stage s: 64 lse then 64 delta
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sQ0 + QST * 2 * C::QT + QST * 512);
   uint64_t* kv_full = bars;
   uint64_t* q_full = bars + 1;          // [QST]
   uint64_t* q_empty = bars + 1 + QST;   // [QST]
   uint64_t* sdp_full = bars + 1 + 2 * QST;  // [2]
   uint64_t* sdp_free = sdp_full + 2;        // [2]
   uint64_t* p_full = sdp_full + 4;          // [2]
-  uint64_t* mm_done = sdp_full + 6;         // [2]
   uint64_t* all_done = sdp_full + 8;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sdp_full + 9);
-  // TMEM columns: buffer g: S^T [128g, 128g+64), dP^T [128g+64, 128g+128);
+  // TMEM columns: buffer g: S^T [128g, 128g+64) -> P^T bf16 in [128g, 128g+32),
+  //               dP^T [128g+64, 128g+128) -> dS^T bf16 in [128g+64, 128g+96);
   //               dV [256, 256+Dh), dK [256+Dh, 256+2Dh)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bh = blockIdx.x, kt = blockIdx.y;
@@ -382,7 +382,6 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
       mbar_init(&sdp_full[g], 1);
       mbar_init(&sdp_free[g], 128);
       mbar_init(&p_full[g], 128);
-      mbar_init(&mm_done[g], 1);
     }
     mbar_init(all_done, 1);
     fence_mbar_init();
@@ -450,13 +449,12 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
         TRACE_MMA(it, 11);
         tc_fence_after();
         const uint32_t aQ = smem_u32(sQ0 + st * 2 * C::QT), aO = aQ + C::QT;
-        const uint32_t aP = smem_u32(sPD + 2 * g * C::PB), aD = aP + C::PB;
+        const uint32_t tP = tmem + g * 128, tD = tP + 64;  // P^T / dS^T as TMEM A operands
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {  // 64 queries / 16
-          tc_mma_f16(tmem + 256, kdesc(aP, ks, 128), mndesc(aO, ks, 64), idesc_g, (it > 0 || ks > 0));
-          tc_mma_f16(tmem + 256 + Dh, kdesc(aD, ks, 128), mndesc(aQ, ks, 64), idesc_g, (it > 0 || ks > 0));
+          tc_mma_f16_ts(tmem + 256, tP + 8 * ks, mndesc(aO, ks, 64), idesc_g, (it > 0 || ks > 0));
+          tc_mma_f16_ts(tmem + 256 + Dh, tD + 8 * ks, mndesc(aQ, ks, 64), idesc_g, (it > 0 || ks > 0));
         }
-        tc_commit(&mm_done[g]);
         tc_commit(&q_empty[st]);
         if (it + 2 < n_it) issue_sdp(it + 2);
       }
@@ -467,7 +465,6 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
     const int r = wq * 32 + lane;  // key row in the tile
     const int key = kt * 128 + r;
     const uint32_t tl = tmem + ((uint32_t)(wq * 32) << 16) + g * 128;
-    const uint32_t aP = smem_u32(sPD + 2 * g * C::PB), aD = aP + C::PB;
     for (int it = g; it < n_it; it += 2) {
       const int st = it % QST, qi = q0 + it, u = it >> 1;
       TRACE(it, 0);
@@ -516,15 +513,20 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
           }
         }
         TRACE(it, 4);
-        if (hf == 0 && u > 0) mbar_wait(&mm_done[g], (u - 1) & 1);  // dV/dK(it - 2) read this buffer
-        TRACE(it, 5);
+        // P^T / dS^T (bf16 pairs) over the S^T / dP^T columns just read; the
+        // dV/dK MMAs of tile it - 2 that read this buffer completed before
+        // this tile's S^T / dP^T MMAs (in-order tensor pipe)
+        uint32_t pk[16], dk[16];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          st_shared_v4(aP + kmaj_off(r, hf * 4 + v, 128), pack8(sv + 8 * v));
-          st_shared_v4(aD + kmaj_off(r, hf * 4 + v, 128), pack8(dp + 8 * v));
+        for (int i = 0; i < 16; ++i) {
+          pk[i] = pack_bf16x2(sv[2 * i], sv[2 * i + 1]);
+          dk[i] = pack_bf16x2(dp[2 * i], dp[2 * i + 1]);
         }
+        tmem_st_32x32b_x16(tl + hf * 16, pk);
+        tmem_st_32x32b_x16(tl + 64 + hf * 16, dk);
+        TRACE(it, 5);
       }
-      fence_proxy_async_smem();
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&p_full[g]);
       TRACE(it, 6);
@@ -565,16 +567,16 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
 
 // ========================================================= backward: dQ ====
 // CTA = 128 queries, 384 threads; two compute warpgroups ping-pong over the
-// 64-key tiles exactly as in dkdv_tc (S / dP double-buffered in TMEM, dS in
-// shared memory); K / V stream through a KST-deep ring.
+// 64-key tiles exactly as in dkdv_tc (S / dP double-buffered in TMEM; dS is
+// written back as bf16 over its dP columns and is the TMEM A operand of
+// dQ += dS K); K / V stream through a KST-deep ring.
 template <int Dh>
 struct Dq {
   static constexpr int DC = Dh / 64;
   static constexpr int KST = 4;
   static constexpr uint32_t QT = 128 * Dh * 2;  // Q / dO tile (128 queries)
   static constexpr uint32_t KT = 64 * Dh * 2;   // K / V tile (64 keys)
-  static constexpr uint32_t DB = 128 * 64 * 2;  // dS tile
-  static constexpr size_t SMEM = 1024 + 2 * QT + KST * 2 * KT + 2 * DB + 512;
+  static constexpr size_t SMEM = 1024 + 2 * QT + KST * 2 * KT + 512;
 };
 
 template <int Dh, bool CAUSAL>
@@ -589,18 +591,17 @@ dq_tc(const __grid_constant__ CUtensorMap map_q128, const __grid_constant__ CUte
   uint8_t* sQ = smem;
   uint8_t* sO = smem + C::QT;
   uint8_t* sK0 = smem + 2 * C::QT;  // stage s: K at sK0 + 2 s KT, V right after
-  uint8_t* sD0 = sK0 + KST * 2 * C::KT;  // buffer g: dS at sD0 + g DB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sD0 + 2 * C::DB);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sK0 + KST * 2 * C::KT);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;          // [KST]
   uint64_t* kv_empty = bars + 1 + KST;   // [KST]
   uint64_t* sdp_full = bars + 1 + 2 * KST;  // [2]
   uint64_t* sdp_free = sdp_full + 2;        // [2]
   uint64_t* p_full = sdp_full + 4;          // [2]
-  uint64_t* mm_done = sdp_full + 6;         // [2]
   uint64_t* all_done = sdp_full + 8;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sdp_full + 9);
-  // TMEM: buffer g: S [128g, 128g+64), dP [128g+64, 128g+128); dQ [256, 256+Dh)
+  // TMEM: buffer g: S [128g, 128g+64), dP [128g+64, 128g+128) -> dS bf16 in
+  //       [128g+64, 128g+96); dQ [256, 256+Dh)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bh = blockIdx.x, qt = gridDim.y - 1 - blockIdx.y;
   const int b = bh / H, h = bh % H;
@@ -622,7 +623,6 @@ dq_tc(const __grid_constant__ CUtensorMap map_q128, const __grid_constant__ CUte
       mbar_init(&sdp_full[g], 1);
       mbar_init(&sdp_free[g], 128);
       mbar_init(&p_full[g], 128);
-      mbar_init(&mm_done[g], 1);
     }
     mbar_init(all_done, 1);
     fence_mbar_init();
@@ -681,11 +681,10 @@ dq_tc(const __grid_constant__ CUtensorMap map_q128, const __grid_constant__ CUte
         const int st = it % KST, g = it & 1;
         mbar_wait(&p_full[g], (it >> 1) & 1);
         tc_fence_after();
-        const uint32_t aK = smem_u32(sK0 + st * 2 * C::KT), aD = smem_u32(sD0 + g * C::DB);
+        const uint32_t aK = smem_u32(sK0 + st * 2 * C::KT), tD = tmem + g * 128 + 64;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks)
-          tc_mma_f16(tmem + 256, kdesc(aD, ks, 128), mndesc(aK, ks, 64), idesc_q, (it > 0 || ks > 0));
-        tc_commit(&mm_done[g]);
+          tc_mma_f16_ts(tmem + 256, tD + 8 * ks, mndesc(aK, ks, 64), idesc_q, (it > 0 || ks > 0));
         tc_commit(&kv_empty[st]);
         if (it + 2 < n_it) issue_sdp(it + 2);
       }
@@ -696,12 +695,10 @@ dq_tc(const __grid_constant__ CUtensorMap map_q128, const __grid_constant__ CUte
     const int r = wq * 32 + lane;
     const int q = qt * 128 + r;
     const uint32_t tl = tmem + ((uint32_t)(wq * 32) << 16) + g * 128;
-    const uint32_t aD = smem_u32(sD0 + g * C::DB);
     const int64_t li = ((int64_t)b * H + h) * S + q;
     const float lse2 = lse[li] * kLog2e, dl = delta[li];
     for (int it = g; it < n_it; it += 2) {
-      const int u = it >> 1;
-      mbar_wait(&sdp_full[g], u & 1);
+      mbar_wait(&sdp_full[g], (it >> 1) & 1);
       tc_fence_after();
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
@@ -726,11 +723,12 @@ dq_tc(const __grid_constant__ CUtensorMap map_q128, const __grid_constant__ CUte
             dp[i] = p * (dp[i] - dl);
           }
         }
-        if (hf == 0 && u > 0) mbar_wait(&mm_done[g], (u - 1) & 1);  // dQ(it - 2) read this buffer
+        uint32_t dk[16];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) st_shared_v4(aD + kmaj_off(r, hf * 4 + v, 128), pack8(dp + 8 * v));
+        for (int i = 0; i < 16; ++i) dk[i] = pack_bf16x2(dp[2 * i], dp[2 * i + 1]);
+        tmem_st_32x32b_x16(tl + 64 + hf * 16, dk);
       }
-      fence_proxy_async_smem();
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&p_full[g]);
     }
