@@ -75,10 +75,14 @@ enum bp_option {
   BP_OPT_LN_UNFUSED = 8,     /* 1: LayerNorm bwd as dx kernel + column kernels
                                 (default 0: one fused launch)                */
   BP_OPT_LN_CTAS_PER_SM = 9, /* fused LayerNorm bwd: row blocks per SM (1..8) */
-  BP_OPT_LN_BWD_MODE = 10    /* bf16 LayerNorm bwd at h in {1024,2048,4096}:
+  BP_OPT_LN_BWD_MODE = 10,   /* bf16 LayerNorm bwd at h in {1024,2048,4096}:
                                 0 (default) two-pass fused kernel, 1 single-
                                 pass TMA-staged kernel (measured 6% slower
                                 cold in the train step, equal L2-warm)      */
+  BP_OPT_ATTN_FWD_MODE = 11,  /* tcgen05 attention fwd: 0 (default) auto
+                                (two query tiles per CTA when S % 256 == 0
+                                and, if causal, at least one tile pair per
+                                SM), 1 one tile per CTA, 2 two tiles        */
 };
 BP_API int bp_set_option(int option, int value);
 

@@ -28,6 +28,7 @@ namespace bp {
 void count_launch();
 int num_sms();
 bool opt_attn_no_tc();
+int attn_fwd_mode();
 int make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, int64_t ld, uint32_t box_inner,
              uint32_t box_outer);
 
@@ -232,15 +233,18 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       tc_fence_before();
       mbar_arrive(&s_free[st]);
       TRACE(32 + j, 2);
-      float mx = -INFINITY;
       const bool diag = CAUSAL && (j == qt);
+      float m8[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) m8[e] = -INFINITY;
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
         float v = s[i] * scale_log2;
         if (diag && hh * 64 + i > r) v = -INFINITY;
         s[i] = v;
-        mx = fmaxf(mx, v);
+        m8[i & 7] = fmaxf(m8[i & 7], v);
       }
+      float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
       float* xs = sX + (j & 1) * 256;
       xs[hh * 128 + r] = mx;
       named_bar_sync(1 + wq, 64);
@@ -267,13 +271,15 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
         m_used = mx;
       }
       TRACE(32 + j, 4);
-      float lsum = 0.f;
+      float l8[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) l8[e] = 0.f;
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
         s[i] = ex2(s[i] - m_used);
-        lsum += s[i];
+        l8[i & 7] += s[i];
       }
-      l += lsum;
+      l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
       TRACE(32 + j, 5);
       if (!waited) mbar_wait(pv_done, (j - 1) & 1);
       TRACE(32 + j, 6);
@@ -308,6 +314,242 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// ================================================ forward, two Q tiles ====
+// CTA = two 128-row query tiles A = 2t, B = 2t + 1 of one (batch, head),
+// 352 threads: warp 0 TMA, warp 1 TMEM allocator + MMA issuer of tile A,
+// warp 2 MMA issuer of tile B, warps 3-6 softmax of A, warps 7-10 softmax of
+// B (warp w owns TMEM lane quarter w & 3 = 32 query rows, whole 128-key score
+// rows per thread).  K / V tiles are loaded once for both query tiles, on
+// separate K and V rings (a K slot frees when both S MMAs are done, a V slot
+// when both P V MMAs are).  The two tiles are independent pipelines, so
+// while group A exponentiates S_A(j) the tensor pipe runs tile B's MMAs.  P
+// is written back as bf16 over the S columns it came from and is the TMEM A
+// operand of O += P V; shared memory only holds Q / K / V.  TMEM: S_A
+// [0,128), S_B [128,256), O_A [256, 256+Dh), O_B [256+Dh, 256+2Dh).
+template <int Dh>
+struct Fwd2 {
+  static constexpr int DC = Dh / 64;
+  static constexpr uint32_t TILE = 128 * Dh * 2;
+  static constexpr size_t SMEM = 1024 + 2 * TILE + 4 * TILE + 512;  // Q_A, Q_B, 2 x (K, V)
+};
+
+template <int Dh, bool CAUSAL>
+__global__ void __launch_bounds__(352, 1)
+fwd2_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ o, float* __restrict__ lse, int S,
+        int H, float scale_log2) {
+  using C = Fwd2<Dh>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;  // tile X at sQ + X * TILE
+  uint8_t* sKV = smem + 2 * C::TILE;  // stage s: K at sKV + 2 s TILE, V right after
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * C::TILE);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;    // [2] ring slots
+  uint64_t* k_empty = bars + 3;   // [2]
+  uint64_t* v_full = bars + 5;    // [2]
+  uint64_t* v_empty = bars + 7;   // [2]
+  uint64_t* s_full = bars + 9;    // [2] per query tile
+  uint64_t* p_full = bars + 11;   // [2]
+  uint64_t* o_done = bars + 13;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bh = blockIdx.x, t = gridDim.y - 1 - blockIdx.y;
+  const int b = bh / H, h = bh % H;
+  const int n_all = S / 128;
+  const int nA = CAUSAL ? 2 * t + 1 : n_all, nB = CAUSAL ? 2 * t + 2 : n_all;
+  const int HD = H * Dh;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_qkv);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 2);  // one commit per query tile
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 2);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&o_done[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------ producer
+#pragma unroll
+      for (int X = 0; X < 2; ++X) {
+        const int qrow = b * S + (2 * t + X) * 128;
+#pragma unroll
+        for (int c = 0; c < C::DC; ++c)
+          tma_load_2d(sQ + X * C::TILE + c * 16384, &map_qkv, h * Dh + c * 64, qrow, q_full);
+      }
+      mbar_expect_tx(q_full, 2 * C::TILE);
+      for (int j = 0; j < nB; ++j) {
+        const int st = j & 1, ph = ((j >> 1) & 1) ^ 1;
+        const int krow = b * S + j * 128;
+        uint8_t* sk = sKV + st * 2 * C::TILE;
+        mbar_wait(&k_empty[st], ph);
+        TRACE_MMA(32 + j, 13);
+#pragma unroll
+        for (int c = 0; c < C::DC; ++c) tma_load_2d(sk + c * 16384, &map_qkv, HD + h * Dh + c * 64, krow, &k_full[st]);
+        mbar_expect_tx(&k_full[st], C::TILE);
+        mbar_wait(&v_empty[st], ph);
+        TRACE_MMA(32 + j, 14);
+#pragma unroll
+        for (int c = 0; c < C::DC; ++c)
+          tma_load_2d(sk + C::TILE + c * 16384, &map_qkv, 2 * HD + h * Dh + c * 64, krow, &v_full[st]);
+        mbar_expect_tx(&v_full[st], C::TILE);
+      }
+    }
+  } else if (warp <= 2) {
+    if (lane == 0) {  // ------------------------ MMA issuer of query tile X
+      const int X = warp - 1, n = X ? nB : nA;
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(128, Dh, false, true);
+      const uint32_t aQ = smem_u32(sQ + X * C::TILE);
+      const uint32_t tS = tmem + X * 128, tO = tmem + 256 + X * Dh;
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(&k_full[st], (j >> 1) & 1);
+        TRACE_MMA(32 + j, X ? 12 : 10);
+        tc_fence_after();
+        const uint32_t aK = smem_u32(sKV + st * 2 * C::TILE);
+#pragma unroll
+        for (int ks = 0; ks < Dh / 16; ++ks) tc_mma_f16(tS, kdesc(aQ, ks, 128), kdesc(aK, ks, 128), idesc_s, ks > 0);
+        tc_commit(&s_full[X]);
+        tc_commit(&k_empty[st]);
+      };
+      issue_s(0);
+      for (int j = 0; j < n; ++j) {
+        const int st = j & 1;
+        mbar_wait(&p_full[X], j & 1);
+        TRACE_MMA(32 + j, X ? 11 : 8);
+        mbar_wait(&v_full[st], (j >> 1) & 1);
+        if (!X) TRACE_MMA(32 + j, 9);
+        tc_fence_after();
+        const uint32_t aV = smem_u32(sKV + st * 2 * C::TILE + C::TILE);
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)  // 128 keys / 16
+          tc_mma_f16_ts(tO, tS + 8 * ks, mndesc(aV, ks, 128), idesc_o, (j > 0 || ks > 0));
+        tc_commit(&v_empty[st]);
+        if (j + 1 < n)
+          issue_s(j + 1);
+        else
+          tc_commit(&o_done[X]);
+      }
+    }
+  } else {  // -------------------------------------------- softmax (warps 3-10)
+    const int X = (warp - 3) >> 2, wq = warp & 3;
+    const int r = wq * 32 + lane;  // query row within the tile
+    const int qt = 2 * t + X, n = X ? nB : nA;
+    const uint32_t tl = tmem + ((uint32_t)(wq * 32) << 16);
+    const uint32_t tS = tl + X * 128, tO = tl + 256 + X * Dh;
+    float m_used = -INFINITY, l = 0.f;  // m_used in the scaled (log2) domain
+    for (int j = 0; j < n; ++j) {
+      if (threadIdx.x == 96) TRACE_MMA(32 + j, 0);
+      mbar_wait(&s_full[X], j & 1);
+      if (threadIdx.x == 96) TRACE_MMA(32 + j, 1);
+      tc_fence_after();
+      // registers hold half a score row at a time (the group's 10 warps
+      // allocate as 12, so 168 registers per thread): pass 1 takes the row
+      // max over two 64-column loads, pass 2 reloads, exponentiates and
+      // writes P back over the first 64 columns
+      const bool diag = CAUSAL && j == qt;
+      // 8 independent max / sum accumulators: a single running fmaxf / fadd
+      // is a 128-long dependency chain (~4 cycles per link)
+      float m8[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) m8[e] = -INFINITY;
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        float s[64];
+        tmem_ld_32x32b_x32_pair(tS + 64 * hf, tS + 64 * hf + 32, *reinterpret_cast<float(*)[32]>(s),
+                                *reinterpret_cast<float(*)[32]>(s + 32));
+        if (diag) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) m8[i & 7] = fmaxf(m8[i & 7], 64 * hf + i > r ? -INFINITY : s[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) m8[i & 7] = fmaxf(m8[i & 7], s[i]);
+        }
+      }
+      const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                             fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      if (threadIdx.x == 96) TRACE_MMA(32 + j, 2);
+      const float mxs = mx * scale_log2;
+      if (mxs > m_used + 8.f) {
+        if (j > 0) {  // O_X holds PV(j-1) complete: S_X(j) was issued after it
+          const float f = ex2(m_used - mxs);
+#pragma unroll 1
+          for (int c = 0; c < Dh / 32; ++c) {
+            float ov[32];
+            tmem_ld_32x32b_x32(tO + c * 32, ov);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) ov[i] *= f;
+            tmem_st_32x32b_x32(tO + c * 32, ov);
+          }
+          l *= f;
+        }
+        m_used = mxs;
+      }
+      if (threadIdx.x == 96) TRACE_MMA(32 + j, 3);
+      float l8[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) l8[e] = 0.f;
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        float s[64];
+        tmem_ld_32x32b_x32_pair(tS + 64 * hf, tS + 64 * hf + 32, *reinterpret_cast<float(*)[32]>(s),
+                                *reinterpret_cast<float(*)[32]>(s + 32));
+        if (diag) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) s[i] = 64 * hf + i > r ? 0.f : ex2(fmaf(s[i], scale_log2, -m_used));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) s[i] = ex2(fmaf(s[i], scale_log2, -m_used));
+        }
+#pragma unroll
+        for (int i = 0; i < 64; ++i) l8[i & 7] += s[i];
+        float pk[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pk[i] = __uint_as_float(pack_bf16x2(s[2 * i], s[2 * i + 1]));
+        // P columns [32 hf, 32 hf + 32) overwrite S columns already read
+        tmem_st_32x32b_x32(tS + 32 * hf, pk);
+      }
+      l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
+      if (threadIdx.x == 96) TRACE_MMA(32 + j, 4);
+      tc_fence_before();
+      mbar_arrive(&p_full[X]);
+      if (threadIdx.x == 96) TRACE_MMA(32 + j, 5);
+    }
+    mbar_wait(&o_done[X], 0);
+    tc_fence_after();
+    const int q = qt * 128 + r;
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* orow = o + ((int64_t)b * S + q) * HD + h * Dh;
+#pragma unroll 1
+    for (int c = 0; c < Dh / 32; ++c) {
+      float ov[32];
+      tmem_ld_32x32b_x32(tO + c * 32, ov);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) ov[i] *= inv;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(orow + c * 32 + 8 * u) = pack8(ov + 8 * u);
+    }
+    lse[((int64_t)b * H + h) * S + q] = (m_used + log2f(l)) * kLn2;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
 // =================================================== backward: dK, dV ====
@@ -796,6 +1038,24 @@ template <int Dh, bool CAUSAL>
 static int fwd(int B, int S, int H, float scale, const void* qkv, void* o, float* lse, cudaStream_t st) {
   CUtensorMap m;
   if (int rc = make_map(&m, qkv, 3ull * H * Dh, (uint64_t)B * S, 3LL * H * Dh, 64, 128)) return rc;
+  // two query tiles per CTA, unless causal with fewer tile pairs than SMs:
+  // the longest pair (2 x 16 key tiles at S = 2048) then bounds the launch and
+  // one-tile CTAs (twice as many, heaviest first) finish sooner (measured at
+  // B=1, H=16: 38.5 vs 55.8 us; at H=32: 71.4 vs 58.8 us)
+  const bool two = S % 256 == 0 && (!CAUSAL || (int64_t)B * H * (S / 256) >= num_sms());
+  const int mode = attn_fwd_mode();
+  if (mode == 2 || (mode == 0 && two && S % 256 == 0)) {
+    auto k2 = fwd2_tc<Dh, CAUSAL>;
+    static bool once2 = false;
+    if (!once2) {
+      if (int rc = set_smem(k2, Fwd2<Dh>::SMEM)) return rc;
+      once2 = true;
+    }
+    k2<<<dim3(B * H, S / 256), 352, Fwd2<Dh>::SMEM, st>>>(m, (__nv_bfloat16*)o, lse, S, H, scale * kLog2e);
+    count_launch();
+    BP_CHECK_LAUNCH("attn_fwd2_tc");
+    return BP_OK;
+  }
   auto k = fwd_tc<Dh, CAUSAL>;
   static bool once = false;
   if (!once) {

@@ -13,14 +13,14 @@ import threading
 __all__ = ["lib", "GemmArgs", "check", "LIB_PATH", "BP_F32", "BP_BF16", "EPI_NONE", "EPI_GELU", "EPI_DGELU",
            "OPT_ATTN_EXACT", "OPT_GEMM_SIMT", "OPT_GEMM_MODE",
            "OPT_STREAM_K", "OPT_GEMM_WIDE", "OPT_GEMM_DEBUG", "OPT_GEMM_TMA_STORE", "OPT_LN_UNFUSED",
-           "OPT_LN_BWD_MODE"]
+           "OPT_LN_BWD_MODE", "OPT_ATTN_FWD_MODE"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "libbitpipe_b200.so")
 
 BP_F32, BP_BF16 = 0, 1
 EPI_NONE, EPI_GELU, EPI_DGELU = 0, 1, 2
 OPT_ATTN_EXACT, OPT_GEMM_SIMT, OPT_GEMM_MODE, OPT_STREAM_K, OPT_GEMM_WIDE = 1, 2, 3, 4, 5
-OPT_GEMM_DEBUG, OPT_GEMM_TMA_STORE, OPT_LN_UNFUSED, OPT_LN_BWD_MODE = 6, 7, 8, 10
+OPT_GEMM_DEBUG, OPT_GEMM_TMA_STORE, OPT_LN_UNFUSED, OPT_LN_BWD_MODE, OPT_ATTN_FWD_MODE = 6, 7, 8, 10, 11
 ABI_VERSION = 2
 
 _vp = ctypes.c_void_p

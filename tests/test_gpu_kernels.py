@@ -285,7 +285,19 @@ def _attn_ref(qkv, B, S, H, Dh, causal, scale):
 @pytest.mark.parametrize("B,S,H,Dh,causal", [(2, 32, 4, 16, True), (1, 256, 2, 64, False), (1, 384, 2, 128, True),
                                              (2, 128, 3, 64, True), (1, 2048, 2, 128, True), (2, 512, 2, 64, False),
                                              (1, 200, 2, 128, True), (1, 136, 1, 64, False)])
-def test_attention(dtype, B, S, H, Dh, causal):
+@pytest.mark.parametrize("fwd_mode", [0, 1, 2], ids=["fwd-auto", "fwd-1tile", "fwd-2tile"])
+def test_attention(dtype, B, S, H, Dh, causal, fwd_mode):
+    from paper_2410_19367_b200.runtime.lib import OPT_ATTN_FWD_MODE
+    if fwd_mode and (dtype != torch.bfloat16 or S % 256):
+        pytest.skip("forward tile mode only applies to the tcgen05 path at S % 256 == 0")
+    ops.set_option(OPT_ATTN_FWD_MODE, fwd_mode)
+    try:
+        _check_attention(dtype, B, S, H, Dh, causal)
+    finally:
+        ops.set_option(OPT_ATTN_FWD_MODE, 0)
+
+
+def _check_attention(dtype, B, S, H, Dh, causal):
     scale = 1.0 / math.sqrt(Dh)
     qkv = torch.randn(B * S, 3 * H * Dh, device="cuda").to(dtype)
     o = torch.empty(B * S, H * Dh, device="cuda", dtype=dtype)

@@ -40,13 +40,14 @@ for i in range(32):
     rel = [row[k] - row[0] if row[k] else 0 for k in (8, 9, 10, 11, 12)]
     print(f"{i:4d} " + " ".join(f"{x:8d}" for x in d) + " | " + " ".join(f"{x:8d}" for x in rel))
 
-# forward kernel, CTA (0,0) = last query tile (16 key tiles), rows 32..47
-names = ["s_full", "ld+arr", "max+xchg", "rescale", "exp+sum", "pv_wait", "st+arr", "->next"]
-print("fwd  " + " ".join(f"{n:>8s}" for n in names) + " | rel: S_iss PV_iss KV_load")
+# forward (two-tile kernel), CTA (0,0) = last query-tile pair, rows 32..47;
+# tile-A softmax warp (thread 96) phases, MMA issue points, producer loads
+names = ["s_full", "max", "rescale", "exp+st", "arrive", "->next"]
+print("fwd  " + " ".join(f"{n:>8s}" for n in names) + " | rel: PVA_p PVA_v S_A(j) PVB_p S_B(j) K(j) V(j)")
 for j in range(16):
     row = t[32 + j]
     if row[0] == 0:
         break
-    d = [row[k + 1] - row[k] for k in range(7)] + [(t[33 + j][0] - row[7]) if j < 15 and t[33 + j][0] else 0]
-    rel = [row[k] - row[0] if row[k] else 0 for k in (8, 9, 10)]
-    print(f"{j:4d} " + " ".join(f"{x:8d}" for x in d) + " | " + " ".join(f"{x:8d}" for x in rel))
+    d = [row[k + 1] - row[k] for k in range(5)] + [(t[33 + j][0] - row[5]) if j < 15 and t[33 + j][0] else 0]
+    rel = [row[k] - row[0] if row[k] else 0 for k in (8, 9, 10, 11, 12, 13, 14)]
+    print(f"{j:4d} " + " ".join(f"{x:8d}" for x in d) + " | " + " ".join(f"{x:7d}" for x in rel))
