@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--paper-policy", action="store_true",
                     help="use the F2 LayoutPolicy order that reaches the analytic bubble")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--partition", default="balanced", choices=["balanced", "uniform"],
+                    help="layer -> stage split: cost-balanced for the schedule (model.balanced_counts) or uniform")
     return ap.parse_args()
 
 
@@ -182,7 +184,7 @@ def main():
         sched = ps.build_bitpipe(D, N, 2, approach is ps.ApproachId.BITPIPE_EARLY_FORWARD, policy=policy)
     else:
         sched = ps.build(approach, D, N)
-    tr = Trainer(cfg, sched, dtype=torch.bfloat16, optim=OptimConfig(), dist_ctx=dist_ctx)
+    tr = Trainer(cfg, sched, dtype=torch.bfloat16, optim=OptimConfig(), dist_ctx=dist_ctx, partition=args.partition)
     tok, tgt = synthetic_batch(cfg, N, seed=1234)
     tok_h = tok.int().pin_memory()
     tgt_h = tgt.int().pin_memory()
@@ -289,6 +291,7 @@ def main():
                                    + (" all logical devices co-resident on 1 GPU" if G == 1 else ""),
                        "global_batch": N * cfg.micro_batch, "seq_len": cfg.seq, "layers": cfg.layers,
                        "hidden": cfg.hidden, "vocab": cfg.vocab, "parallelism": f"pp{D} bidirectional",
+                       "partition": {"kind": args.partition, "halfblocks_per_stage": tr.partition},
                        "l2": "working set (2.6 GB weights, GBs of activations) >> 126 MB L2"},
             "loss_mean": loss_mean,
             "e2e": e2e,

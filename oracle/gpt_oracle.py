@@ -188,7 +188,7 @@ def sequential_baseline(cfg: OracleConfig, params: dict, tokens, targets, *, dty
 
 
 def run_schedule_numeric(cfg: OracleConfig, schedule_json: str | dict, params: dict, tokens, targets, *,
-                         dtype=torch.float64, adam_state=None, step: int = 1) -> StepResult:
+                         dtype=torch.float64, adam_state=None, step: int = 1, halfblocks=None) -> StepResult:
     """Execute the reference per-device orders with message passing.
 
     Workers advance in lock-step rounds: a device runs its next task when
@@ -202,7 +202,10 @@ def run_schedule_numeric(cfg: OracleConfig, schedule_json: str | dict, params: d
     dirs = [m["direction"] for m in sch["stage_maps"]]
     N = tokens.shape[0]
     n_rep = N // len(dirs)  # micro-batches per replica
-    hbs = stage_halfblocks(cfg.layers, S_tot)
+    # partition: the uniform rule, or an explicit per-stage half-block list
+    # (the product's cost-balanced partition); the result is the same model
+    hbs = [list(h) for h in halfblocks] if halfblocks is not None else stage_halfblocks(cfg.layers, S_tot)
+    assert len(hbs) == S_tot and [hb for h in hbs for hb in h] == list(range(2 * cfg.layers))
     replicas = {d: _clone_params(params, dtype) for d in dirs}
     rows = [[tuple(r[:4]) for r in dev] for dev in sch["per_device"]]
     pos = [0] * D

@@ -28,7 +28,8 @@ from dataclasses import dataclass, field
 
 import torch
 
-__all__ = ["ModelConfig", "CONFIGS", "StagePlan", "stage_partition", "param_specs", "stage_param_names",
+__all__ = ["ModelConfig", "CONFIGS", "StagePlan", "stage_partition", "balanced_counts", "stage_costs",
+           "device_loads", "param_specs", "stage_param_names",
            "init_params", "flops_per_token"]
 
 
@@ -90,26 +91,111 @@ class StagePlan:
     head: bool
 
 
-def stage_partition(cfg: ModelConfig, num_stages: int) -> tuple[StagePlan, ...]:
+def stage_partition(cfg: ModelConfig, num_stages: int, counts=None) -> tuple[StagePlan, ...]:
     """Contiguous split of the 2L half-blocks over ``num_stages`` stages.
 
-    Remainders go to the middle stages first (the end stages already carry
-    the embedding / LM head).  Every stage gets >= 0 half-blocks; stages
-    with none still pass activations through (and own embed/head if ends).
+    Default (uniform): remainders go to the middle stages first (the end
+    stages already carry the embedding / LM head).  ``counts`` gives the
+    number of half-blocks per stage explicitly (e.g. :func:`balanced_counts`).
+    Every stage gets >= 0 half-blocks; stages with none still pass
+    activations through (and own embed/head if ends).
     """
     n = 2 * cfg.layers
-    base, rem = divmod(n, num_stages)
-    extra = [0] * num_stages
-    order = sorted(range(num_stages), key=lambda s: (abs(2 * s - (num_stages - 1)), s))
-    for s in order[:rem]:
-        extra[s] = 1
+    if counts is None:
+        base, rem = divmod(n, num_stages)
+        extra = [0] * num_stages
+        order = sorted(range(num_stages), key=lambda s: (abs(2 * s - (num_stages - 1)), s))
+        for s in order[:rem]:
+            extra[s] = 1
+        counts = [base + e for e in extra]
+    counts = [int(c) for c in counts]
+    if len(counts) != num_stages or min(counts) < 0 or sum(counts) != n:
+        raise ValueError(f"partition counts {counts} do not split {n} half-blocks over {num_stages} stages")
     plans, start = [], 0
     for s in range(num_stages):
-        cnt = base + extra[s]
-        plans.append(StagePlan(s, tuple(range(start, start + cnt)), s == 0, s == num_stages - 1))
-        start += cnt
-    assert start == n
+        plans.append(StagePlan(s, tuple(range(start, start + counts[s])), s == 0, s == num_stages - 1))
+        start += counts[s]
     return tuple(plans)
+
+
+def _hb_flops(cfg: ModelConfig, hb: int) -> float:
+    """Forward FLOPs per token of half-block ``hb`` (attention or MLP half)."""
+    h, s = cfg.hidden, cfg.seq
+    if hb % 2 == 0:  # QKV + out-projection GEMMs, attention scores / context
+        return 8.0 * h * h + 4.0 * s * h * (0.5 if cfg.causal else 1.0)
+    return 4.0 * h * cfg.ffn  # fc1 + fc2
+
+
+def stage_costs(cfg: ModelConfig, counts) -> list[float]:
+    """Forward FLOPs per token of each stage: its half-blocks plus the LM
+    head (2 V h) on the last stage; the embedding gather is free."""
+    out, start = [], 0
+    for s, c in enumerate(counts):
+        f = sum(_hb_flops(cfg, hb) for hb in range(start, start + c))
+        if s == len(counts) - 1:
+            f += 2.0 * cfg.vocab * cfg.hidden
+        out.append(f)
+        start += c
+    return out
+
+
+def device_loads(cfg: ModelConfig, counts, stage_maps) -> list[float]:
+    """Per-device compute of one direction-symmetric partition: every
+    direction's stage map places the same stages (same partition, one model
+    replica per direction) on its devices (schedules.py:58-108 StageMap)."""
+    cost = stage_costs(cfg, counts)
+    D = max(max(m.assignment) for m in stage_maps) + 1
+    loads = [0.0] * D
+    for m in stage_maps:
+        for st, d in enumerate(m.assignment):
+            loads[d] += cost[st]
+    return loads
+
+
+def balanced_counts(cfg: ModelConfig, schedule) -> list[int]:
+    """Half-blocks per stage for a cost-balanced partition (SURVEY §7 step
+    3): the stage that also computes the LM head (~2 V h FLOPs per token,
+    3-4 half-blocks at GPT sizes) gets fewer half-blocks.
+
+    Objective: the makespan of the reference ASAP replay (``list_schedule``,
+    fusion.py:34-77) of ``schedule``'s fixed per-device orders with task
+    durations F = stage FLOPs, B = 2 x F (one GPU per logical device, free
+    communication), then the most loaded device, then the spread of device
+    loads.  Local search from the uniform split, moving one half-block
+    across a stage boundary at a time while the objective improves; the
+    result depends only on (cfg, schedule) and is deterministic."""
+    from fractions import Fraction
+
+    from .schedule import list_schedule
+
+    S = schedule.num_stages
+    maps = [schedule.stage_map(d) for d in schedule.directions]
+    counts = [len(p.halfblocks) for p in stage_partition(cfg, S)]
+    unit = 1e6
+
+    def score(c):
+        cost = [Fraction(round(x / unit)) for x in stage_costs(cfg, c)]
+        dur = lambda t: cost[t.stage] * (1 if t.kind.value == "F" else 2)  # noqa: E731
+        starts = list_schedule(schedule.per_device, schedule.dependencies, dur)
+        mk = max(st + dur(t) for t, st in starts.items())
+        ld = device_loads(cfg, c, maps)
+        return (mk, max(ld), sum(x * x for x in ld))
+
+    best = score(counts)
+    improved = True
+    while improved:
+        improved = False
+        for b in range(S - 1):
+            for delta in (1, -1):  # one half-block from stage b to b+1, or back
+                c = list(counts)
+                c[b] -= delta
+                c[b + 1] += delta
+                if min(c) < 0:
+                    continue
+                sc = score(c)
+                if sc < best:
+                    best, counts, improved = sc, c, True
+    return counts
 
 
 def param_specs(cfg: ModelConfig):

@@ -34,7 +34,7 @@ from dataclasses import dataclass
 
 import torch
 
-from ..model import CONFIGS, ModelConfig, OptimConfig, stage_partition
+from ..model import CONFIGS, ModelConfig, OptimConfig, balanced_counts, stage_partition
 from ..schedule import Direction, Schedule, TaskKind, canonical_replay
 from . import ops
 from .compute import StageCompute
@@ -107,7 +107,7 @@ class Trainer:
 
     def __init__(self, cfg: ModelConfig, schedule: Schedule, *, dtype=torch.bfloat16, optim: OptimConfig | None = None,
                  params: dict | None = None, seed: int = 1234, device=None, dist_ctx=None, record_timeline=False,
-                 serial_streams: bool = False):
+                 serial_streams: bool = False, partition="uniform"):
         if not torch.cuda.is_available():
             raise RuntimeError("BitPipe Trainer needs a CUDA device (no CPU fallback)")
         ops.lib()  # fail loudly now if the kernel library is missing
@@ -120,7 +120,16 @@ class Trainer:
         self.dirs = list(schedule.directions)
         self.bidir = len(self.dirs) == 2
         self.n_rep = self.N // len(self.dirs)
-        self.plans = stage_partition(cfg, self.S)
+        # layer -> stage partition: "uniform", "balanced" (cost-balanced for
+        # this schedule, model.balanced_counts) or explicit half-blocks per stage
+        if partition == "uniform":
+            counts = None
+        elif partition == "balanced":
+            counts = balanced_counts(cfg, schedule)
+        else:
+            counts = list(partition)
+        self.plans = stage_partition(cfg, self.S, counts)
+        self.partition = [len(p.halfblocks) for p in self.plans]
         self.dist = dist_ctx
         self.device = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
         torch.cuda.set_device(self.device)
