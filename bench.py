@@ -33,9 +33,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "GPT tokens/sec/box at D=1/2/4/8 B200 (frac of roofline); bubble fraction"
-# ncu --set full, fc1 forward GEMM 2048x8192x2048 (profiles/r1_ncu_full_summary.txt):
+# ncu --set full, fc1 forward GEMM 2048x8192x2048 (profiles/r1b_ncu_full_summary.txt):
 # dram__bytes_read.sum + dram__bytes_write.sum per launch
-TRAFFIC_FC1_BYTES = 42.026496e6 + 2.713344e6
+TRAFFIC_FC1_BYTES = 42.101504e6 + 6.494720e6
 
 
 def parse():
@@ -306,7 +306,7 @@ def main():
                          "share_of_step": gemm_share, "fc1_fprop_avg_us": fc1_us,
                          "peak_kind": f"{peak_kind} sustained (kernel timed inside a long step)",
                          "traffic_note": "dram read+write bytes per fc1-fprop launch from ncu --set full "
-                                         "(profiles/r1_ncu_full_summary.txt)"},
+                                         "(profiles/r1b_ncu_full_summary.txt)"},
             "step_roofline": {"tokens_per_s": roof_tps, "frac": value / roof_tps, "F_tok": F_tok,
                               "peak_tflops": peak_sust, "peak_kind": f"{peak_kind} sustained",
                               "beta_ideal": beta_ideal, "model_tflops": value * F_tok / 1e12},
