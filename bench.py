@@ -48,8 +48,11 @@ def parse():
     ap.add_argument("--approach", default="bitpipe")
     ap.add_argument("--D", type=int, default=None)
     ap.add_argument("--N", type=int, default=16)
-    ap.add_argument("--paper-policy", action="store_true",
-                    help="use the F2 LayoutPolicy order that reaches the analytic bubble")
+    ap.add_argument("--order", default="paper", choices=["paper", "default"],
+                    help="BitPipe order: 'paper' = the F2 LayoutPolicy order (SURVEY §0 F2; bit-exact vs the "
+                         "reference engine under that policy; reaches the analytic bubble) where one is known for "
+                         "D, else the reference default; 'default' = build_bitpipe's default policy")
+    ap.add_argument("--paper-policy", action="store_true", help="alias of --order paper")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--partition", default="balanced", choices=["balanced", "uniform"],
                     help="layer -> stage split: cost-balanced for the schedule (model.balanced_counts) or uniform")
@@ -179,7 +182,8 @@ def main():
         D = args.D or 8
     N = args.N
     approach = ps.ApproachId.parse(args.approach)
-    policy = ps.paper_policy(D) if args.paper_policy else None
+    use_paper = (args.order == "paper" or args.paper_policy) and D in ps.PAPER_GATE_STAGE
+    policy = ps.paper_policy(D) if use_paper and approach is ps.ApproachId.BITPIPE else None
     if approach in (ps.ApproachId.BITPIPE, ps.ApproachId.BITPIPE_EARLY_FORWARD):
         sched = ps.build_bitpipe(D, N, 2, approach is ps.ApproachId.BITPIPE_EARLY_FORWARD, policy=policy)
     else:
@@ -253,6 +257,8 @@ def main():
     beta_ideal = float(ps.analytic_bubble_ratio(approach, D, N)) if G > 1 else 0.0
     roof_tps = G * peak_sust * 1e12 * (1 - beta_ideal) / F_tok
     beta_order = float(ps.canonical_bubble(sched))
+    beta_default_order = (float(ps.canonical_bubble(ps.build_bitpipe(D, N))) if approach is ps.ApproachId.BITPIPE
+                          else beta_order)
     # dominant kernel: the tcgen05 GEMM.  Live: CUDA events around every GEMM
     # launch (on its own stream) during one extra step after the timed region,
     # with the logical devices' work serialised on one stream so that a
@@ -312,6 +318,8 @@ def main():
                               "beta_ideal": beta_ideal, "model_tflops": value * F_tok / 1e12},
             "bubble": {"analytic": float(ps.analytic_bubble_ratio(approach, D, N)),
                        "canonical_of_order": beta_order,
+                       "order": "F2 paper policy" if policy else "reference default",
+                       "canonical_of_reference_default_order": beta_default_order,
                        "measured_replay": replay,
                        "note": "1 GPU: the D logical devices share the GPU, so pipeline bubbles are filled by other "
                                "streams; measured_replay = ASAP replay of the executed per-device orders with each "

@@ -118,22 +118,34 @@ def stage_partition(cfg: ModelConfig, num_stages: int, counts=None) -> tuple[Sta
     return tuple(plans)
 
 
+# Cost model of the partitioner, in GEMM-equivalent FLOPs per token,
+# calibrated on B200 (tools/stage_times.py, GPT-1.3B D=8: attention half :
+# MLP half : LM head = 1 : 1 : 2.9 in measured task time, B / F = 1.98):
+# attention-core FLOPs run at ~0.45x the GEMMs' rate, the LM-head GEMMs
+# (N = V) at ~1.5x, and the fused cross-entropy moves 3 V 2-byte values per
+# token at HBM speed (~6.5 TB/s vs ~1 PFLOP/s of GEMM).
+ATTN_CORE_WEIGHT = 2.3
+HEAD_GEMM_WEIGHT = 0.6
+XENT_FLOPS_PER_BYTE = 1000.0 / 6.5
+
+
 def _hb_flops(cfg: ModelConfig, hb: int) -> float:
-    """Forward FLOPs per token of half-block ``hb`` (attention or MLP half)."""
+    """Forward cost per token of half-block ``hb`` (attention or MLP half)."""
     h, s = cfg.hidden, cfg.seq
     if hb % 2 == 0:  # QKV + out-projection GEMMs, attention scores / context
-        return 8.0 * h * h + 4.0 * s * h * (0.5 if cfg.causal else 1.0)
+        return 8.0 * h * h + ATTN_CORE_WEIGHT * 4.0 * s * h * (0.5 if cfg.causal else 1.0)
     return 4.0 * h * cfg.ffn  # fc1 + fc2
 
 
 def stage_costs(cfg: ModelConfig, counts) -> list[float]:
-    """Forward FLOPs per token of each stage: its half-blocks plus the LM
-    head (2 V h) on the last stage; the embedding gather is free."""
+    """Forward cost per token of each stage (see the cost-model constants):
+    its half-blocks plus, on the last stage, the LM head and the fused
+    softmax cross-entropy; the embedding gather is free."""
     out, start = [], 0
     for s, c in enumerate(counts):
         f = sum(_hb_flops(cfg, hb) for hb in range(start, start + c))
         if s == len(counts) - 1:
-            f += 2.0 * cfg.vocab * cfg.hidden
+            f += HEAD_GEMM_WEIGHT * 2.0 * cfg.vocab * cfg.hidden + XENT_FLOPS_PER_BYTE * 3 * cfg.vocab * 2
         out.append(f)
         start += c
     return out
