@@ -63,6 +63,20 @@ class StageCompute:
         self.M = cfg.micro_batch * cfg.seq
         self.grad_scale = grad_scale          # d(step objective)/d(micro-batch mean loss)
         self.loss_scale = 1.0 / self.M
+        self.wgrad_beta = 1.0                 # 0.0 for the first backward of an iteration
+        # cross-stage bias-gradient fusion (coresident executor): the output
+        # gradient of this stage IS the dx of the next stage's last LayerNorm
+        # backward, which accumulates its column sums into this stage's last
+        # output-projection bias gradient (``prev_out_bias`` of the next stage)
+        self.prev_out_bias = None
+        self.out_bias_by_next = False
+
+    def begin_iteration(self):
+        """The next backward is this replica's first of the iteration: its
+        weight-gradient GEMMs write (beta = 0) instead of accumulating, which
+        replaces zeroing the (large) GEMM-weight part of the gradient buffer.
+        All backwards of one replica run on one stream, in issue order."""
+        self.wgrad_beta = 0.0
 
     # ------------------------------------------------------------- forward --
     def forward(self, stream, pool: BufferPool, *, x0=None, tokens=None, targets=None, loss_slot=None):
@@ -130,21 +144,23 @@ class StageCompute:
         H, Dh = cfg.heads, cfg.head_dim
         scale = 1.0 / math.sqrt(Dh)
         release = st.buffers()
+        wb, self.wgrad_beta = self.wgrad_beta, 1.0
         if self.plan.head:
             xf, mean, rstd, dlogits = st.head
             dxf = pool.get((M, h), dt, stream)
             ops.gemm(dlogits, P["head.lm.w"], dxf, b_kmajor=False, stream=stream)
-            ops.gemm(dlogits, xf, G["head.lm.w"], a_kmajor=False, b_kmajor=False, beta=1.0, stream=stream)
+            ops.gemm(dlogits, xf, G["head.lm.w"], a_kmajor=False, b_kmajor=False, beta=wb, stream=stream)
             dy = pool.get((M, h), dt, stream)
             # the LN backward also sums its dx over rows: that is the output-bias
             # gradient of the half-block before it (fused, no separate launch)
             ops.layernorm_bwd(dxf, st.xs[-1], P["head.lnf.w"], mean, rstd, dy, G["head.lnf.w"], G["head.lnf.b"],
-                              dx_colsum=self._out_bias_grad(len(self.plan.halfblocks) - 1), stream=stream)
+                              dx_colsum=(self._out_bias_grad(len(self.plan.halfblocks) - 1) if self.plan.halfblocks
+                                         else self.prev_out_bias), stream=stream)
             bias_done = bool(self.plan.halfblocks)
             release += [dxf, dy]
         else:
             release.append(dy)
-            bias_done = False
+            bias_done = self.out_bias_by_next
         for i in range(len(self.plan.halfblocks) - 1, -1, -1):
             l, half = divmod(self.plan.halfblocks[i], 2)
             p = f"layers.{l}."
@@ -153,7 +169,7 @@ class StageCompute:
             dx = pool.get((M, h), dt, stream)
             if half == 0:
                 _, a, mean, rstd, qkv, o, lse = save
-                ops.gemm(dy, o, G[p + "attn.proj.w"], a_kmajor=False, b_kmajor=False, beta=1.0, stream=stream)
+                ops.gemm(dy, o, G[p + "attn.proj.w"], a_kmajor=False, b_kmajor=False, beta=wb, stream=stream)
                 if not bias_done:
                     ops.colsum_acc(dy, G[p + "attn.proj.b"], stream=stream)
                 do = pool.get((M, h), dt, stream)
@@ -163,15 +179,15 @@ class StageCompute:
                 # attention backward's epilogues
                 ops.attn_bwd(qkv, o, do, lse, dqkv, ws, cfg.micro_batch, cfg.seq, H, Dh, cfg.causal, scale,
                              stream=stream, dbias=G[p + "attn.qkv.b"])
-                ops.gemm(dqkv, a, G[p + "attn.qkv.w"], a_kmajor=False, b_kmajor=False, beta=1.0, stream=stream)
+                ops.gemm(dqkv, a, G[p + "attn.qkv.w"], a_kmajor=False, b_kmajor=False, beta=wb, stream=stream)
                 da = pool.get((M, h), dt, stream)
                 ops.gemm(dqkv, P[p + "attn.qkv.w"], da, b_kmajor=False, stream=stream)
                 ops.layernorm_bwd(da, x, P[p + "ln1.w"], mean, rstd, dx, G[p + "ln1.w"], G[p + "ln1.b"], dres=dy,
-                                  dx_colsum=self._out_bias_grad(i - 1), stream=stream)
+                                  dx_colsum=self._out_bias_grad(i - 1) if i else self.prev_out_bias, stream=stream)
                 release += [do, dqkv, da]
             else:
                 _, m, mean, rstd, u, g = save
-                ops.gemm(dy, g, G[p + "mlp.fc2.w"], a_kmajor=False, b_kmajor=False, beta=1.0, stream=stream)
+                ops.gemm(dy, g, G[p + "mlp.fc2.w"], a_kmajor=False, b_kmajor=False, beta=wb, stream=stream)
                 if not bias_done:
                     ops.colsum_acc(dy, G[p + "mlp.fc2.b"], stream=stream)
                 du = pool.get((M, cfg.ffn), dt, stream)
@@ -179,11 +195,11 @@ class StageCompute:
                 # gradient) are reduced in the same GEMM epilogue
                 ops.gemm(dy, P[p + "mlp.fc2.w"], du, b_kmajor=False, aux=u, epilogue=EPI_DGELU, stream=stream,
                          colsum=G[p + "mlp.fc1.b"])
-                ops.gemm(du, m, G[p + "mlp.fc1.w"], a_kmajor=False, b_kmajor=False, beta=1.0, stream=stream)
+                ops.gemm(du, m, G[p + "mlp.fc1.w"], a_kmajor=False, b_kmajor=False, beta=wb, stream=stream)
                 dm = pool.get((M, h), dt, stream)
                 ops.gemm(du, P[p + "mlp.fc1.w"], dm, b_kmajor=False, stream=stream)
                 ops.layernorm_bwd(dm, x, P[p + "ln2.w"], mean, rstd, dx, G[p + "ln2.w"], G[p + "ln2.b"], dres=dy,
-                                  dx_colsum=self._out_bias_grad(i - 1), stream=stream)
+                                  dx_colsum=self._out_bias_grad(i - 1) if i else self.prev_out_bias, stream=stream)
                 release += [du, dm]
             if i > 0 or self.plan.embed:
                 release.append(dx)

@@ -153,6 +153,13 @@ class Trainer:
                 sp.load(params)
                 self.stage_params[(dr, s)] = sp
                 self.compute[(dr, s)] = StageCompute(cfg, self.plans[s], sp, grad_scale=grad_scale)
+        if dist_ctx is None:  # all stages local: fuse each stage's last output-bias gradient
+            for dr in self.dirs:  # into the next stage's message-producing LayerNorm backward
+                for s in range(1, self.S):
+                    prev, cur = self.compute[(dr, s - 1)], self.compute[(dr, s)]
+                    if prev.plan.halfblocks and (cur.plan.halfblocks or cur.plan.head):
+                        cur.prev_out_bias = prev._out_bias_grad(len(prev.plan.halfblocks) - 1)
+                        prev.out_bias_by_next = True
         # optimizer state: one master/m/v per stage present locally (coresident:
         # shared by the two replicas; distributed: per local replica)
         self.opt_owner: dict = {}
@@ -189,10 +196,15 @@ class Trainer:
         return self.sched.stage_map(dr).device_of(s)
 
     def _zero_grads(self):
+        """Zero the atomically accumulated gradients; the GEMM-written weight
+        gradients are overwritten by each stage replica's first backward of
+        the iteration (StageCompute.begin_iteration)."""
         for (dr, s), sp in self.stage_params.items():
             st = self.streams[self._dev_of(dr, s)]
             with torch.cuda.stream(st):
-                sp.grad.zero_()
+                sp.grad[:sp.zero_numel].zero_()
+        for comp in self.compute.values():
+            comp.begin_iteration()
 
     def _adam(self, stage_key, grads, params_out, stream, grad_scale=1.0):
         owner = self.opt_owner[stage_key]

@@ -22,18 +22,32 @@ __all__ = ["StageParams", "BufferPool", "ALIGN"]
 ALIGN = 64
 
 
+GEMM_WEIGHTS = ("attn.qkv.w", "attn.proj.w", "mlp.fc1.w", "mlp.fc2.w", "head.lm.w")
+
+
 class StageParams:
     """Flat storage of one stage replica's parameters and gradients."""
 
     def __init__(self, cfg: ModelConfig, plan: StagePlan, dtype: torch.dtype, device):
         shapes = {n: s for n, s, _ in param_specs(cfg)}
-        self.names = stage_param_names(plan)
+        # GEMM-written weight gradients last: the first backward of an
+        # iteration writes them (beta = 0) instead of accumulating, so only the
+        # leading atomically-accumulated part (embeddings, biases, LayerNorm)
+        # needs zeroing before the iteration (``zero_numel``)
+        names = stage_param_names(plan)
+        self.names = ([n for n in names if not n.endswith(GEMM_WEIGHTS)] +
+                      [n for n in names if n.endswith(GEMM_WEIGHTS)])
         self.offsets = {}
         off = 0
+        self.zero_numel = None
         for n in self.names:
+            if self.zero_numel is None and n.endswith(GEMM_WEIGHTS):
+                self.zero_numel = off
             self.offsets[n] = off
             off += -(-math.prod(shapes[n]) // ALIGN) * ALIGN
         self.numel = max(off, ALIGN)
+        if self.zero_numel is None:
+            self.zero_numel = self.numel
         self.dtype = dtype
         self.device = torch.device(device)
         self.flat = torch.zeros(self.numel, dtype=dtype, device=device)
