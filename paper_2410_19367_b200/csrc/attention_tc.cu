@@ -417,6 +417,10 @@ fwd2_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__
       const uint32_t aQ = smem_u32(sQ + X * C::TILE);
       const uint32_t tS = tmem + X * 128, tO = tmem + 256 + X * Dh;
       mbar_wait(q_full, 0);
+      // tile B starts half a period behind tile A, so one group exponentiates
+      // while the other's MMAs run (in lock-step both would contend for the
+      // MUFU and then leave the tensor pipe idle together)
+      if (X == 1 && n > 1) mbar_wait(&p_full[0], 0);
       auto issue_s = [&](int j) {
         const int st = j & 1;
         mbar_wait(&k_full[st], (j >> 1) & 1);

@@ -20,6 +20,8 @@ o = torch.empty(B * S, H * Dh, device="cuda", dtype=torch.bfloat16)
 lse = torch.empty(B * H * S, device="cuda")
 dq = torch.empty_like(qkv)
 ws = torch.empty(ops.attn_workspace_numel(B, S, H, Dh), device="cuda")
+from paper_2410_19367_b200.runtime.lib import OPT_ATTN_FWD_MODE
+ops.set_option(OPT_ATTN_FWD_MODE, int(os.environ.get("FWD_MODE", "2")))  # trace the two-tile forward
 for _ in range(3):
     ops.attn_fwd(qkv, o, lse, B, S, H, Dh, True, 1 / math.sqrt(Dh))
     ops.attn_bwd(qkv, o, o, lse, dq, ws, B, S, H, Dh, True, 1 / math.sqrt(Dh))
