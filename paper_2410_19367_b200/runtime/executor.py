@@ -257,7 +257,7 @@ class Trainer:
             dx, release = self.compute[(t.direction, t.stage)].backward(stream, self.pool, stash, dy, self.ws[d])
             ev = torch.cuda.Event(enable_timing=tl is not None)
             ev.record(stream)
-            self.pool.put_all(release, ev)
+            self.pool.put_all(release, ev, stream)
             if tl is not None:
                 tl.append((d, t, e0, ev))
             return dx, ev

@@ -96,10 +96,18 @@ class BufferPool:
         self.allocated_bytes = 0
 
     def get(self, shape, dtype, stream):
+        """A free buffer of this shape, preferring one released on ``stream``
+        itself (stream order already covers its last use, no cross-stream
+        dependency); otherwise the most recently released one, after making
+        ``stream`` wait for its release event."""
         key = (tuple(shape), dtype)
         lst = self.free[key]
         if lst:
-            t, ev = lst.pop()
+            sid = stream.cuda_stream
+            for i in range(len(lst) - 1, -1, -1):
+                if lst[i][2] == sid:
+                    return lst.pop(i)[0]
+            t, ev, _ = lst.pop()
             if ev is not None:
                 stream.wait_event(ev)
             return t
@@ -108,7 +116,9 @@ class BufferPool:
         self.allocated_bytes += t.numel() * t.element_size()
         return t
 
-    def put_all(self, tensors, event) -> None:
+    def put_all(self, tensors, event, stream=None) -> None:
+        """Release ``tensors`` once ``event`` (recorded on ``stream``) fires."""
+        sid = stream.cuda_stream if stream is not None else None
         for t in tensors:
             if t is not None:
-                self.free[(tuple(t.shape), t.dtype)].append((t, event))
+                self.free[(tuple(t.shape), t.dtype)].append((t, event, sid))
