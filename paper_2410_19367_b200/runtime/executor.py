@@ -107,7 +107,7 @@ class Trainer:
 
     def __init__(self, cfg: ModelConfig, schedule: Schedule, *, dtype=torch.bfloat16, optim: OptimConfig | None = None,
                  params: dict | None = None, seed: int = 1234, device=None, dist_ctx=None, record_timeline=False,
-                 serial_streams: bool = False, partition="uniform"):
+                 serial_streams: bool = False, partition="uniform", stream_priority=None):
         if not torch.cuda.is_available():
             raise RuntimeError("BitPipe Trainer needs a CUDA device (no CPU fallback)")
         ops.lib()  # fail loudly now if the kernel library is missing
@@ -175,7 +175,9 @@ class Trainer:
             one = torch.cuda.Stream(device=self.device)
             self.streams = {d: one for d in self.local_devices}
         else:
-            self.streams = {d: torch.cuda.Stream(device=self.device) for d in self.local_devices}
+            prio = self._stream_priorities(stream_priority)
+            self.streams = {d: torch.cuda.Stream(device=self.device, priority=prio.get(d, 0))
+                            for d in self.local_devices}
         self.opt_stream = torch.cuda.Stream(device=self.device)
         self.pool = BufferPool(self.device)
         wsn = ops.attn_workspace_numel(cfg.micro_batch, cfg.seq, cfg.heads, cfg.head_dim)
@@ -192,6 +194,24 @@ class Trainer:
         self.timeline = None
 
     # ----------------------------------------------------------------- helpers --
+    def _stream_priorities(self, mode) -> dict:
+        """Co-resident CUDA stream priorities (lower = more urgent).  'tail':
+        the logical devices whose lists finish last in the canonical replay
+        get the highest priority, so the pipeline drain (few streams with work
+        left) is shorter; None / 'none': all equal."""
+        import os
+        mode = mode or os.environ.get("BP_STREAM_PRIORITY")
+        if mode in (None, "", "none") or len(self.local_devices) < 2:
+            return {}
+        if mode != "tail":
+            raise ValueError(f"unknown stream_priority {mode!r}")
+        starts, _ = canonical_replay(self.sched)
+        end = {d: max(starts[t] + self.sched.canonical_duration(t) for t in row)
+               for d, row in enumerate(self.sched.per_device)}
+        ranked = sorted(self.local_devices, key=lambda d: (-end[d], d))
+        levels = sorted(set(end[d] for d in ranked), reverse=True)
+        return {d: -max(0, 2 - levels.index(end[d])) for d in ranked}  # 3 levels: -2, -1, 0
+
     def _dev_of(self, dr: Direction, s: int) -> int:
         return self.sched.stage_map(dr).device_of(s)
 

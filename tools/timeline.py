@@ -11,7 +11,10 @@ from paper_2410_19367_b200.runtime.executor import Trainer
 
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "gpt-1.3b"]
 D, N = 8, 16
-tr = Trainer(cfg, ps.build_bitpipe(D, N), dtype=torch.bfloat16, optim=OptimConfig(), record_timeline=True)
+import os
+pol = ps.paper_policy(D) if os.environ.get("ORDER", "paper") == "paper" else None
+tr = Trainer(cfg, ps.build_bitpipe(D, N, policy=pol), dtype=torch.bfloat16, optim=OptimConfig(), record_timeline=True,
+             partition=os.environ.get("PARTITION", "balanced"))
 tok, tgt = synthetic_batch(cfg, N)
 tok, tgt = tok.int().cuda(), tgt.int().cuda()
 import time
@@ -39,3 +42,21 @@ for a, b in spans:
 union += cur_b - cur_a
 print(f"makespan {info['makespan_ms']:.1f} ms; sum of task spans {busy_sum:.1f} ms; union {union:.1f} ms; "
       f"mean concurrency {busy_sum / union:.2f}; per-device busy ms {[round(v, 1) for v in info['busy_ms'].values()]}")
+
+# time-weighted distribution of the number of tasks in flight (a task's span
+# runs from its first kernel's start event to its end event on its stream)
+ev = sorted([(a, 1) for a, b in spans] + [(b, -1) for a, b in spans])
+hist, k, last = {}, 0, ev[0][0]
+t0, t1 = ev[0][0], ev[-1][0]
+edges = []
+for t, dk in ev:
+    hist[k] = hist.get(k, 0.0) + (t - last)
+    edges.append((last, t, k))
+    k += dk
+    last = t
+tot = t1 - t0
+print("in-flight tasks: " + ", ".join(f"{kk}: {100 * v / tot:.1f}%" for kk, v in sorted(hist.items())))
+for lo, hi in ((0.0, 0.1), (0.1, 0.9), (0.9, 1.0)):
+    a, b = t0 + lo * tot, t0 + hi * tot
+    w = sum(max(0.0, min(e, b) - max(s, a)) * kk for s, e, kk in edges)
+    print(f"  mean in-flight over [{lo:.0%}, {hi:.0%}] of the step: {w / (b - a):.2f}")
