@@ -109,9 +109,9 @@ BP_DEV uint64_t mndesc(uint32_t base, int ks, int krows) {
 template <int Dh>
 struct Fwd {
   static constexpr int DC = Dh / 64;
+  static constexpr int KS = 3;  // K ring depth (a K slot frees when S is done, a V slot only after P V)
   static constexpr uint32_t TILE = 128 * Dh * 2;
-  static constexpr uint32_t PB = 128 * 128 * 2;
-  static constexpr size_t SMEM = 1024 + TILE + 4 * TILE + PB + 2048 + 512;
+  static constexpr size_t SMEM = 1024 + TILE + KS * TILE + 2 * TILE + 2048 + 512;
 };
 
 template <int Dh, bool CAUSAL>
@@ -119,22 +119,27 @@ __global__ void __launch_bounds__(384, 1)
 fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ o, float* __restrict__ lse, int S,
        int H, float scale_log2) {
   using C = Fwd<Dh>;
+  constexpr int KS = C::KS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sK[2] = {smem + C::TILE, smem + 3 * C::TILE};
-  uint8_t* sV[2] = {smem + 2 * C::TILE, smem + 4 * C::TILE};
-  uint8_t* sP = smem + 5 * C::TILE;
-  float* sX = reinterpret_cast<float*>(sP + C::PB);  // [2 parity][2 halves][128 rows] partial row maxima
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::PB + 2048);
+  uint8_t* sK0 = smem + C::TILE;              // K slot s at sK0 + s TILE
+  uint8_t* sV0 = sK0 + KS * C::TILE;          // V slot s at sV0 + s TILE
+  float* sX = reinterpret_cast<float*>(sV0 + 2 * C::TILE);  // [2 parity][2 halves][128 rows] partial maxima
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV0 + 2 * C::TILE + 2048);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* s_free = bars + 7;    // [2]
-  uint64_t* p_full = bars + 9;
-  uint64_t* pv_done = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  uint64_t* k_full = bars + 1;        // [KS]
+  uint64_t* k_empty = bars + 1 + KS;  // [KS]
+  uint64_t* v_full = bars + 1 + 2 * KS;   // [2]
+  uint64_t* v_empty = v_full + 2;         // [2]
+  uint64_t* s_full = v_full + 4;          // [2]
+  uint64_t* s_free = v_full + 6;          // [2]
+  uint64_t* p_full = v_full + 8;
+  uint64_t* pv_done = v_full + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_full + 10);
+  // TMEM: S buffers [0,128) and [128,256) (P of tile j is written back as bf16
+  // over the first 64 columns of its S buffer: the TMEM A operand of O += P V),
+  // O [256, 256+Dh)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bh = blockIdx.x, qt = gridDim.y - 1 - blockIdx.y;
@@ -145,9 +150,13 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
   if (warp == 0 && lane == 0) tma_prefetch_desc(&map_qkv);
   if (warp == 1 && lane == 0) {
     mbar_init(q_full, 1);
+    for (int i = 0; i < KS; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], 256);
     }
@@ -167,50 +176,65 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
 #pragma unroll
       for (int c = 0; c < C::DC; ++c) tma_load_2d(sQ + c * 16384, &map_qkv, h * Dh + c * 64, qrow, q_full);
       mbar_expect_tx(q_full, C::TILE);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        TRACE_MMA(32 + j, 10);
-        const int krow = b * S + j * 128;
+      // K runs up to KS tiles ahead, V two; interleave so that neither waits
+      // behind the other's (later) free slot
+      int jk = 0, jv = 0;
+      while (jv < n_kv) {
+        if (jk < n_kv && jk < jv + KS) {
+          const int st = jk % KS;
+          mbar_wait(&k_empty[st], ((jk / KS) & 1) ^ 1);
+          TRACE_MMA(32 + jk, 10);
 #pragma unroll
-        for (int c = 0; c < C::DC; ++c) {
-          tma_load_2d(sK[st] + c * 16384, &map_qkv, HD + h * Dh + c * 64, krow, &kv_full[st]);
-          tma_load_2d(sV[st] + c * 16384, &map_qkv, 2 * HD + h * Dh + c * 64, krow, &kv_full[st]);
+          for (int c = 0; c < C::DC; ++c)
+            tma_load_2d(sK0 + st * C::TILE + c * 16384, &map_qkv, HD + h * Dh + c * 64, b * S + jk * 128, &k_full[st]);
+          mbar_expect_tx(&k_full[st], C::TILE);
+          ++jk;
         }
-        mbar_expect_tx(&kv_full[st], 2 * C::TILE);
+        if (jv < jk - 1 || jk == n_kv) {
+          const int st = jv & 1;
+          mbar_wait(&v_empty[st], ((jv >> 1) & 1) ^ 1);
+#pragma unroll
+          for (int c = 0; c < C::DC; ++c)
+            tma_load_2d(sV0 + st * C::TILE + c * 16384, &map_qkv, 2 * HD + h * Dh + c * 64, b * S + jv * 128,
+                        &v_full[st]);
+          mbar_expect_tx(&v_full[st], C::TILE);
+          ++jv;
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------ MMA issuer
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);
       constexpr uint32_t idesc_o = umma_idesc_bf16(128, Dh, false, true);
-      const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
+      const uint32_t aQ = smem_u32(sQ);
       mbar_wait(q_full, 0);
       tc_fence_after();
       for (int j = 0; j <= n_kv; ++j) {
         if (j < n_kv) {
-          const int st = j & 1;
-          mbar_wait(&kv_full[st], (j >> 1) & 1);
+          const int st = j & 1, ks_ = j % KS;
+          mbar_wait(&k_full[ks_], (j / KS) & 1);
           mbar_wait(&s_free[st], ((j >> 1) & 1) ^ 1);
           TRACE_MMA(32 + j, 8);
           tc_fence_after();
-          const uint32_t aK = smem_u32(sK[st]);
+          const uint32_t aK = smem_u32(sK0 + ks_ * C::TILE);
 #pragma unroll
           for (int ks = 0; ks < Dh / 16; ++ks)
             tc_mma_f16(tmem + st * 128, kdesc(aQ, ks, 128), kdesc(aK, ks, 128), idesc_s, ks > 0);
           tc_commit(&s_full[st]);
+          tc_commit(&k_empty[ks_]);
         }
         if (j >= 1) {
           const int jj = j - 1, st = jj & 1;
           mbar_wait(p_full, jj & 1);
+          mbar_wait(&v_full[st], (jj >> 1) & 1);
           TRACE_MMA(32 + jj, 9);
           tc_fence_after();
-          const uint32_t aV = smem_u32(sV[st]);
+          const uint32_t aV = smem_u32(sV0 + st * C::TILE);
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks)
-            tc_mma_f16(tmem + 256, kdesc(aP, ks, 128), mndesc(aV, ks, 128), idesc_o, (jj > 0 || ks > 0));
+            tc_mma_f16_ts(tmem + 256, tmem + st * 128 + 8 * ks, mndesc(aV, ks, 128), idesc_o, (jj > 0 || ks > 0));
           tc_commit(pv_done);
-          tc_commit(&kv_empty[st]);
+          tc_commit(&v_empty[st]);
         }
       }
     }
@@ -218,7 +242,6 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
     const int wq = warp & 3, hh = (warp - 4) >> 2;
     const int r = wq * 32 + lane;
     const uint32_t tl = tmem + ((uint32_t)(wq * 32) << 16);
-    const uint32_t aP = smem_u32(sP);
     constexpr int OC = Dh / 64;  // 32-column O chunks per half
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < n_kv; ++j) {
@@ -250,11 +273,9 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       named_bar_sync(1 + wq, 64);
       mx = fmaxf(mx, xs[(hh ^ 1) * 128 + r]);
       TRACE(32 + j, 3);
-      bool waited = (j == 0);
       if (mx > m_used + 8.f) {
-        if (j > 0) {
+        if (j > 0) {  // rescale O: needs P V of tile j-1 complete
           mbar_wait(pv_done, (j - 1) & 1);
-          waited = true;
           tc_fence_after();
           const float f = ex2(m_used - mx);
 #pragma unroll 1
@@ -281,11 +302,14 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       }
       l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
       TRACE(32 + j, 5);
-      if (!waited) mbar_wait(pv_done, (j - 1) & 1);
-      TRACE(32 + j, 6);
+      // P (bf16 pairs) over this half's 32 of the S buffer's first 64 columns
+      // (already read by both halves: s_free); P V of tile j-2 that read this
+      // buffer completed before S(j) (in-order tensor pipe)
+      float pk[32];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) st_shared_v4(aP + kmaj_off(r, hh * 8 + u, 128), pack8(s + 8 * u));
-      fence_proxy_async_smem();
+      for (int i = 0; i < 32; ++i) pk[i] = __uint_as_float(pack_bf16x2(s[2 * i], s[2 * i + 1]));
+      TRACE(32 + j, 6);
+      tmem_st_32x32b_x32(tl + st * 128 + hh * 32, pk);
       tc_fence_before();
       mbar_arrive(p_full);
       TRACE(32 + j, 7);
