@@ -80,9 +80,9 @@ enum bp_option {
                                 pass TMA-staged kernel (measured 6% slower
                                 cold in the train step, equal L2-warm)      */
   BP_OPT_ATTN_FWD_MODE = 11,  /* tcgen05 attention fwd: 0 (default) auto
-                                (two query tiles per CTA when S % 256 == 0
-                                and, if causal, at least one tile pair per
-                                SM), 1 one tile per CTA, 2 two tiles        */
+                                (two query tiles per CTA for non-causal
+                                attention at S % 256 == 0, else one), 1 one
+                                tile per CTA, 2 two tiles                   */
 };
 BP_API int bp_set_option(int option, int value);
 
