@@ -254,10 +254,18 @@ __global__ void adam_kernel(int64_t n, float* __restrict__ master, const float* 
     reinterpret_cast<float4*>(master)[i] = make_float4(ww[0], ww[1], ww[2], ww[3]);
     reinterpret_cast<float4*>(m)[i] = make_float4(m4[0], m4[1], m4[2], m4[3]);
     reinterpret_cast<float4*>(v)[i] = make_float4(v4[0], v4[1], v4[2], v4[3]);
+    if (sizeof(P) == 2) {  // 4 bf16 working-copy values = one 8-byte store per replica
+      uint2 u;
+      *reinterpret_cast<__nv_bfloat162*>(&u.x) = __floats2bfloat162_rn(ww[0], ww[1]);
+      *reinterpret_cast<__nv_bfloat162*>(&u.y) = __floats2bfloat162_rn(ww[2], ww[3]);
+      if (pa) reinterpret_cast<uint2*>(pa)[i] = u;
+      if (pb) reinterpret_cast<uint2*>(pb)[i] = u;
+    } else {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (pa) pa[4 * i + j] = from_f<P>(ww[j]);
-      if (pb) pb[4 * i + j] = from_f<P>(ww[j]);
+      for (int j = 0; j < 4; ++j) {
+        if (pa) pa[4 * i + j] = from_f<P>(ww[j]);
+        if (pb) pb[4 * i + j] = from_f<P>(ww[j]);
+      }
     }
   }
   // tail
