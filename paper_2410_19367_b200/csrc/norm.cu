@@ -61,38 +61,54 @@ __global__ void __launch_bounds__(256) ln_fwd_warp(int rows, const T* __restrict
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= rows) return;
   const typename V::U* xr = reinterpret_cast<const typename V::U*>(x + (int64_t)row * cols);
-  typename V::U pv[NV];
-  float s = 0.f;
+  const typename V::U* gr = reinterpret_cast<const typename V::U*>(g);
+  const typename V::U* br = reinterpret_cast<const typename V::U*>(b);
+  // gamma / beta are requested together with the row so their latency hides
+  // behind the reductions; E independent partial sums per lane instead of
+  // one 64-long dependent add chain
+  typename V::U pv[NV], pg[NV], pb[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) pv[i] = xr[i * 32 + lane];
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
-    pv[i] = xr[i * 32 + lane];
+    pg[i] = gr[i * 32 + lane];
+    pb[i] = br[i * 32 + lane];
+  }
+  float sp[E] = {};
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
     float t[E];
     V::unpack(pv[i], t);
 #pragma unroll
-    for (int j = 0; j < E; ++j) s += t[j];
+    for (int j = 0; j < E; ++j) sp[j] += t[j];
   }
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < E; ++j) s += sp[j];
   const float mu = warp_sum(s) * (1.f / cols);
-  float q = 0.f;
+#pragma unroll
+  for (int j = 0; j < E; ++j) sp[j] = 0.f;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     float t[E];
     V::unpack(pv[i], t);
 #pragma unroll
     for (int j = 0; j < E; ++j) {
-      float d = t[j] - mu;
-      q += d * d;
+      const float d = t[j] - mu;
+      sp[j] = fmaf(d, d, sp[j]);
     }
   }
+  float q = 0.f;
+#pragma unroll
+  for (int j = 0; j < E; ++j) q += sp[j];
   const float rs = rsqrtf(warp_sum(q) * (1.f / cols) + eps);
-  const typename V::U* gr = reinterpret_cast<const typename V::U*>(g);
-  const typename V::U* br = reinterpret_cast<const typename V::U*>(b);
   typename V::U* yr = reinterpret_cast<typename V::U*>(y + (int64_t)row * cols);
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     float gg[E], bb[E], o[E], t[E];
     V::unpack(pv[i], t);
-    V::unpack(gr[i * 32 + lane], gg);
-    V::unpack(br[i * 32 + lane], bb);
+    V::unpack(pg[i], gg);
+    V::unpack(pb[i], bb);
 #pragma unroll
     for (int j = 0; j < E; ++j) o[j] = (t[j] - mu) * rs * gg[j] + bb[j];
     yr[i * 32 + lane] = V::pack(o);
