@@ -66,7 +66,11 @@ enum bp_option {
   BP_OPT_GEMM_MODE = 3,  /* tcgen05 tiling: 0 auto, 1 single-SM, 2 CTA pair    */
   BP_OPT_STREAM_K = 4,   /* stream-K GEMM scheduling: 0 auto (sub-wave, K >= 4096
                             only), 1 every ragged last wave, 2 off (default:
-                            measured slower on the GPT-1.3B shapes)          */
+                            measured slower on the GPT-1.3B shapes).  Testing
+                            aid for a GEMM running ALONE on the GPU: its
+                            owner CTAs spin on contributor CTAs of the same
+                            launch, which can deadlock when kernels of other
+                            streams hold SMs (the co-resident executor)     */
   BP_OPT_GEMM_WIDE = 5,  /* 256 x 512 pair tiles: 1 force (default 0: never,
                             measured slower than 256 x 256)                  */
   BP_OPT_GEMM_DEBUG = 6,  /* 1: skip the GEMM epilogue stores (profiling only) */
