@@ -143,6 +143,67 @@ __global__ void embed_bwd_pos_kernel(int B, int S, int H, const T* __restrict__ 
   }
 }
 
+// 16-byte vector variants (bf16, H % 8 == 0): thread = 8 columns of a row.
+BP_DEV void unpack8(const uint4& u, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 t = __bfloat1622float2(h[j]);
+    f[2 * j] = t.x;
+    f[2 * j + 1] = t.y;
+  }
+}
+
+__global__ void embed_fwd_vec(int S, int H8, const int32_t* __restrict__ tok, const uint4* __restrict__ wte,
+                              const uint4* __restrict__ wpe, uint4* __restrict__ out) {
+  const int r = blockIdx.x, s = r % S;
+  const int64_t t = tok[r];
+  for (int c = threadIdx.x; c < H8; c += blockDim.x) {
+    float a[8], b[8];
+    unpack8(wte[t * H8 + c], a);
+    unpack8(wpe[(int64_t)s * H8 + c], b);
+    uint4 o;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(a[2 * j] + b[2 * j], a[2 * j + 1] + b[2 * j + 1]);
+    out[(int64_t)r * H8 + c] = o;
+  }
+}
+
+__global__ void embed_bwd_tok_vec(int H8, const int32_t* __restrict__ tok, const uint4* __restrict__ dout,
+                                  float* __restrict__ dwte) {
+  const int r = blockIdx.x;
+  const int64_t t = tok[r];
+  for (int c = threadIdx.x; c < H8; c += blockDim.x) {
+    float d[8];
+    unpack8(dout[(int64_t)r * H8 + c], d);
+    float* dst = dwte + (t * H8 + c) * 8;
+    red_add_v4(dst, d[0], d[1], d[2], d[3]);
+    red_add_v4(dst + 4, d[4], d[5], d[6], d[7]);
+  }
+}
+
+__global__ void embed_bwd_pos_vec(int B, int S, int H8, const uint4* __restrict__ dout, float4* __restrict__ dwpe) {
+  const int s = blockIdx.x;
+  for (int c = threadIdx.x; c < H8; c += blockDim.x) {
+    float acc[8] = {};
+    for (int b = 0; b < B; ++b) {
+      float d[8];
+      unpack8(dout[((int64_t)b * S + s) * H8 + c], d);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += d[j];
+    }
+    float4* dst = dwpe + ((int64_t)s * H8 + c) * 2;
+    float4 lo = dst[0], hi = dst[1];
+    lo.x += acc[0]; lo.y += acc[1]; lo.z += acc[2]; lo.w += acc[3];
+    hi.x += acc[4]; hi.y += acc[5]; hi.z += acc[6]; hi.w += acc[7];
+    dst[0] = lo;
+    dst[1] = hi;
+  }
+}
+
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 // --------------------------------------------------------------- xent ----
 // Block per row.  Pass 1: online max / sum-exp over 16-byte vectors.
 // Pass 2: re-read (L2-resident), write the scaled gradient in place.
@@ -309,7 +370,10 @@ extern "C" int bp_embed_fwd(int dtype, int B, int S, int H, const int32_t* token
                             void* out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int threads = H >= 256 ? 256 : 64;
-  if (dtype == BP_F32)
+  if (dtype == BP_BF16 && H % 8 == 0 && al16(wte) && al16(wpe) && al16(out)) {
+    embed_fwd_vec<<<B * S, H / 8 >= 256 ? 256 : 64, 0, st>>>(S, H / 8, tokens, (const uint4*)wte, (const uint4*)wpe,
+                                                              (uint4*)out);
+  } else if (dtype == BP_F32)
     embed_fwd_kernel<float><<<B * S, threads, 0, st>>>(B, S, H, tokens, (const float*)wte, (const float*)wpe,
                                                         (float*)out);
   else
@@ -324,7 +388,11 @@ extern "C" int bp_embed_bwd(int dtype, int B, int S, int H, const int32_t* token
                             float* dwpe, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int threads = H >= 256 ? 256 : 64;
-  if (dtype == BP_F32) {
+  if (dtype == BP_BF16 && H % 8 == 0 && al16(dout) && al16(dwte) && al16(dwpe)) {
+    const int t8 = H / 8 >= 256 ? 256 : 64;
+    embed_bwd_tok_vec<<<B * S, t8, 0, st>>>(H / 8, tokens, (const uint4*)dout, dwte);
+    embed_bwd_pos_vec<<<S, t8, 0, st>>>(B, S, H / 8, (const uint4*)dout, (float4*)dwpe);
+  } else if (dtype == BP_F32) {
     embed_bwd_tok_kernel<float><<<B * S, threads, 0, st>>>(H, tokens, (const float*)dout, dwte);
     embed_bwd_pos_kernel<float><<<S, threads, 0, st>>>(B, S, H, (const float*)dout, dwpe);
   } else {
