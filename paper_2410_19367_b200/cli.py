@@ -14,6 +14,9 @@ executor:
   search    grid over approach x D x N (x order policy), modelled throughput;
             best row last
   render    ASCII slot grid (``scratch_diag.py``) or SVG Gantt of a schedule
+  measure   run the schedule's train step on the B200 (all logical devices
+            co-resident) and export the MEASURED per-task timeline (CUDA
+            events) in the simulate JSON format, or as an SVG Gantt
   verify    structural checks of every requested schedule (validation,
             acyclicity, byte-determinism, per-link message accounting); with
             ``--gpu`` also schedule independence of the B200 train step in the
@@ -352,12 +355,63 @@ def _verify_gpu(scheds, lines, args) -> int:
     return failed
 
 
+def cmd_measure(args) -> int:
+    """Measured timeline of one train step (after warm-up) of ``--model`` on
+    this GPU: per-task start / end in ms from the CUDA events the executor
+    records on each logical device's stream, per-device busy time, makespan
+    and bubble (with co-resident logical devices the bubble
+    describes stream occupancy, not idle GPU time)."""
+    import torch
+    if not torch.cuda.is_available():
+        raise perr.PipeschedError("measure needs a CUDA device")
+    from .model import CONFIGS, OptimConfig, synthetic_batch
+    from .runtime.executor import Trainer
+    model = args.model or "tiny"
+    if model not in CONFIGS:
+        raise UsageError(f"unknown model {model!r} (known: {sorted(CONFIGS)})")
+    cfg = CONFIGS[model]
+    for a in _approaches(args):
+        for D, N in _grid_points(args):
+            s = build_one(a, D, N, args.v, args.early_forward, args.order)
+            tr = Trainer(cfg, s, dtype=torch.bfloat16 if args.dtype == "bf16" else torch.float32,
+                         optim=OptimConfig(), record_timeline=True, partition=args.partition)
+            tok, tgt = synthetic_batch(cfg, N, seed=args.seed)
+            tok, tgt = tok.int().cuda(), tgt.int().cuda()
+            for _ in range(3):
+                tr.train_step(tok, tgt)
+            torch.cuda.synchronize()
+            first = tr.timeline[0][2]
+            tasks, busy = [], [0.0] * D
+            for d, t, e0, e1 in tr.timeline:
+                a0, a1 = first.elapsed_time(e0), first.elapsed_time(e1)
+                busy[d] += a1 - a0
+                tasks.append({"device": d, "kind": t.kind.value, "micro_batch": t.micro_batch, "stage": t.stage,
+                              "direction": t.direction.value, "chunk": t.stage // D,
+                              "start": f"{a0:.4f}", "end": f"{a1:.4f}"})
+            t0 = min(float(x["start"]) for x in tasks)
+            mk = max(float(x["end"]) for x in tasks) - t0
+            for x in tasks:
+                x["start"], x["end"] = f"{float(x['start']) - t0:.4f}", f"{float(x['end']) - t0:.4f}"
+            bubble = 1 - sum(busy) / (D * mk) if mk else 0.0
+            tl = {"approach": s.approach.value, "D": D, "N": N, "v": s.v, "unit": "ms", "model": model,
+                  "partition": tr.partition, "makespan": f"{mk:.4f}", "bubble": f"{bubble:.6f}",
+                  "bubble_float": bubble, "busy": [f"{b:.4f}" for b in busy], "tasks": tasks,
+                  "durations": "measured (CUDA events per task on each logical device's stream; co-resident)"}
+            base = f"{s.approach.value}_D{D}_N{N}_measured"
+            if args.format == "svg":
+                _emit(gantt_svg(tl), args.out, base + ".svg")
+            else:
+                _emit(json.dumps(tl, indent=1, sort_keys=True) + "\n", args.out, base + ".timeline.json")
+    return EXIT_OK
+
+
 def make_parser() -> argparse.ArgumentParser:
     ap = argparse.ArgumentParser(prog="pipesched", description=__doc__.split("\n\n")[0])
     sub = ap.add_subparsers(dest="cmd", required=True)
     for name, fn, fmt in (("plan", cmd_plan, ["json"]), ("compare", cmd_compare, ["csv", "json"]),
                           ("simulate", cmd_simulate, ["json", "svg"]), ("search", cmd_search, ["csv", "json"]),
-                          ("render", cmd_render, ["txt", "svg"]), ("verify", cmd_verify, ["txt"])):
+                          ("render", cmd_render, ["txt", "svg"]), ("verify", cmd_verify, ["txt"]),
+                          ("measure", cmd_measure, ["json", "svg"])):
         p = sub.add_parser(name)
         p.set_defaults(fn=fn)
         p.add_argument("--approach", action="append", help="approach name or alias (repeatable)")
@@ -375,6 +429,8 @@ def make_parser() -> argparse.ArgumentParser:
         p.add_argument("--seed", type=int, default=7)
         if name == "verify":
             p.add_argument("--gpu", action="store_true", help="also run the B200 train-step equivalence suite")
+        if name == "measure":
+            p.add_argument("--dtype", choices=["bf16", "fp32"], default="bf16")
     return ap
 
 

@@ -84,3 +84,20 @@ def test_verify_gpu_schedule_independence(capsys):
     rc, out, _ = run(capsys, "verify", "--gpu", "--approach", "bitpipe", "--approach", "chimera", "--D", "2",
                      "--D", "4")
     assert rc == 0 and out.count("ok   gpu") == 4, out
+
+
+def test_measure_needs_gpu_on_cpu_box(capsys):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    rc, _, err = run(capsys, "measure", "--approach", "bitpipe", "--D", "2", "--N", "4")
+    assert rc == 2 and "CUDA" in err
+
+
+@pytest.mark.gpu
+def test_measure_timeline(capsys):
+    rc, out, _ = run(capsys, "measure", "--approach", "bitpipe", "--D", "4", "--N", "8", "--model", "tiny",
+                     "--dtype", "fp32")
+    tl = json.loads(out)
+    assert rc == 0 and len(tl["tasks"]) == 4 * 4 * 8 and float(tl["makespan"]) > 0
+    assert all(float(t["end"]) >= float(t["start"]) for t in tl["tasks"])
