@@ -53,6 +53,8 @@ def parse():
                          "reference engine under that policy; reaches the analytic bubble) where one is known for "
                          "D, else the reference default; 'default' = build_bitpipe's default policy")
     ap.add_argument("--paper-policy", action="store_true", help="alias of --order paper")
+    ap.add_argument("--replicas", type=int, default=1,
+                    help="data-parallel pipeline replicas W (N>1 only): D = world / W, each replica on its own batch")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--partition", default="balanced", choices=["balanced", "uniform"],
                     help="layer -> stage split: cost-balanced for the schedule (model.balanced_counts) or uniform")
@@ -176,8 +178,8 @@ def main():
     if world > 1:
         from paper_2410_19367_b200.runtime.distributed import DistContext
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-        D = world
-        dist_ctx = DistContext(rank, world)
+        dist_ctx = DistContext(rank, world, replicas=args.replicas)
+        D = dist_ctx.D
     else:
         D = args.D or 8
     N = args.N
@@ -189,7 +191,8 @@ def main():
     else:
         sched = ps.build(approach, D, N)
     tr = Trainer(cfg, sched, dtype=torch.bfloat16, optim=OptimConfig(), dist_ctx=dist_ctx, partition=args.partition)
-    tok, tgt = synthetic_batch(cfg, N, seed=1234)
+    W = dist_ctx.replicas if dist_ctx is not None else 1
+    tok, tgt = synthetic_batch(cfg, N, seed=1234 + (dist_ctx.w if dist_ctx is not None else 0))  # replica's batch
     tok_h = tok.int().pin_memory()
     tgt_h = tgt.int().pin_memory()
     tok_d, tgt_d = tok_h.cuda(), tgt_h.cuda()
@@ -218,7 +221,7 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = t.item()
-    tokens_per_step = N * cfg.micro_batch * cfg.seq
+    tokens_per_step = W * N * cfg.micro_batch * cfg.seq   # whole job: every pipeline replica
     value = tokens_per_step / (ms / 1e3)
     loss_mean = out.losses.float().mean().item()
 
@@ -295,8 +298,8 @@ def main():
             "config": {"workload": f"{cfg.name} {approach.value} v=2 D={D} N={N}"
                                    + (" (F2 paper policy)" if policy else "")
                                    + (" all logical devices co-resident on 1 GPU" if G == 1 else ""),
-                       "global_batch": N * cfg.micro_batch, "seq_len": cfg.seq, "layers": cfg.layers,
-                       "hidden": cfg.hidden, "vocab": cfg.vocab, "parallelism": f"pp{D} bidirectional",
+                       "global_batch": W * N * cfg.micro_batch, "seq_len": cfg.seq, "layers": cfg.layers,
+                       "hidden": cfg.hidden, "vocab": cfg.vocab, "parallelism": f"pp{D} bidirectional" + (f" x dp{W}" if W > 1 else ""),
                        "partition": {"kind": args.partition, "halfblocks_per_stage": tr.partition},
                        "l2": "working set (2.6 GB weights, GBs of activations) >> 126 MB L2"},
             "loss_mean": loss_mean,

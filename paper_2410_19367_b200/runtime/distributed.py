@@ -21,6 +21,13 @@ Eager gradient synchronisation
   grad_scale 1/2 (replica mean).  A 2-term fp32 sum is commutative, so both
   replicas compute bit-identical updates.
 
+Data parallelism over W replicated pipelines (``replicated_pipelines``,
+core.py:68; "stage replicas co-located"): world = W x D, rank
+= w * D + d runs logical device d of pipeline replica w on its own batch;
+P2P stays inside a replica, and the stage group spans the stage's holders
+in every replica (2W ranks bidirectional, W unidirectional), gradient mean
+over all of them.
+
 All of this is host-side control flow; it runs unchanged on CPU tensors with
 the gloo backend (``cuda=False``), which is how tests/ exercise it.
 """
@@ -58,8 +65,13 @@ def link_messages(sched: Schedule) -> dict:
 
 
 class DistContext:
-    def __init__(self, rank: int, world: int, *, cuda: bool = True):
+    def __init__(self, rank: int, world: int, *, cuda: bool = True, replicas: int = 1):
+        if replicas < 1 or world % replicas:
+            raise ValueError(f"world {world} is not a multiple of the pipeline replica count {replicas}")
         self.rank, self.world, self.cuda = rank, world, cuda
+        self.replicas = replicas
+        self.D = world // replicas
+        self.w, self.dev = divmod(rank, self.D)   # pipeline replica, logical device
         self.sched = None
         self.link_group: dict = {}
         self.pair_group: dict = {}
@@ -71,17 +83,23 @@ class DistContext:
     # ----------------------------------------------------------- setup --
     def build_groups(self, sched: Schedule) -> None:
         """Create every group in the same order on every rank."""
-        if sched.D != self.world:
-            raise ValueError(f"distributed mode needs world == D (world={self.world}, D={sched.D})")
+        if sched.D != self.D:
+            raise ValueError(f"distributed mode needs world == replicas x D "
+                             f"(world={self.world}, replicas={self.replicas}, D={sched.D})")
         self.sched = sched
         self.links = link_messages(sched)
-        for (src, dst) in sorted(self.links):
-            self.link_group[(src, dst)] = dist.new_group(sorted({src, dst}))
-        if sched.is_bidirectional:
-            dn, up = sched.stage_maps
-            for s in range(sched.num_stages):
-                a, b = dn.device_of(s), up.device_of(s)
-                self.pair_group[s] = (a, b, dist.new_group(sorted({a, b})))
+        D = self.D
+        # every rank creates every group, in one global order (new_group is collective)
+        for w in range(self.replicas):
+            for (src, dst) in sorted(self.links):
+                g = dist.new_group(sorted({w * D + src, w * D + dst}))
+                if w == self.w:
+                    self.link_group[(src, dst)] = g
+        for s in range(sched.num_stages):
+            devs = sorted({m.device_of(s) for m in sched.stage_maps})
+            members = sorted(w * D + d for w in range(self.replicas) for d in devs)
+            if len(members) > 1:
+                self.pair_group[s] = (members, dist.new_group(members))
         self.warmup()
 
     def warmup(self) -> None:
@@ -96,20 +114,24 @@ class DistContext:
         """
         dev = torch.device("cuda", torch.cuda.current_device()) if self.cuda else torch.device("cpu")
         t = torch.zeros(1, device=dev)
-        for (src, dst) in sorted(self.link_group):
+        for (src, dst) in sorted(self.link_group):  # links never cross replicas: no inter-replica waits
             g = self.link_group[(src, dst)]
-            if self.rank == src:
-                dist.send(t, dst, group=g)
-            elif self.rank == dst:
-                dist.recv(t, src, group=g)
+            if self.dev == src:
+                dist.send(t, self._g(dst), group=g)
+            elif self.dev == dst:
+                dist.recv(t, self._g(src), group=g)
         for s in sorted(self.pair_group):
-            a, b, g = self.pair_group[s]
-            if self.rank in (a, b):
+            members, g = self.pair_group[s]
+            if self.rank in members:
                 dist.all_reduce(t, group=g)
         if self.cuda:
             torch.cuda.synchronize()
 
     # ------------------------------------------------------- primitives --
+    def _g(self, d: int) -> int:
+        """Global rank of logical device ``d`` of this rank's pipeline replica."""
+        return self.w * self.D + d
+
     def _sctx(self, stream):
         return torch.cuda.stream(stream) if (self.cuda and stream is not None) else nullcontext()
 
@@ -118,16 +140,16 @@ class DistContext:
         sender's order.  ``alloc(key) -> tensor`` provides the slot buffer."""
         with self._sctx(stream):
             for (src, dst), keys in sorted(self.links.items()):
-                if dst != self.rank:
+                if dst != self.dev:
                     continue
                 g = self.link_group[(src, dst)]
                 for key in keys:
                     buf = alloc(key)
-                    self.slots[key] = (buf, dist.irecv(buf, src, group=g))
+                    self.slots[key] = (buf, dist.irecv(buf, self._g(src), group=g))
 
     def send(self, key, tensor, dst, stream=None) -> None:
         with self._sctx(stream):
-            work = dist.isend(tensor, dst, group=self.link_group[(self.rank, dst)])
+            work = dist.isend(tensor, self._g(dst), group=self.link_group[(self.dev, dst)])
         self.inflight.append((tensor, work))
 
     def recv(self, key, stream=None):
@@ -139,18 +161,19 @@ class DistContext:
             work.wait()
         return buf
 
-    def allreduce_stage(self, stage: int, tensor, stream=None) -> bool:
-        """SUM-all-reduce ``tensor`` with the other replica of ``stage``;
-        False if the schedule has no replica pair (unidirectional)."""
+    def allreduce_stage(self, stage: int, tensor, stream=None) -> int:
+        """SUM-all-reduce ``tensor`` over every holder of ``stage`` (the other
+        direction's replica, and the same stage in the other pipeline
+        replicas); returns the number of summed copies (1: nothing to do)."""
         if stage not in self.pair_group:
-            return False
+            return 1
+        members, g = self.pair_group[stage]
         with self._sctx(stream):
             if self.cuda:   # NCCL: stream-ordered, the host never blocks
-                dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=self.pair_group[stage][2])
+                dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=g)
             else:           # gloo: host-blocking collectives would serialise ranks; run async
-                self.pending.append(dist.all_reduce(tensor, op=dist.ReduceOp.SUM,
-                                                    group=self.pair_group[stage][2], async_op=True))
-        return True
+                self.pending.append(dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=g, async_op=True))
+        return len(members)
 
     def finish_allreduces(self) -> None:
         for w in self.pending:
@@ -174,7 +197,7 @@ class DistContext:
     def begin_iteration(self, trainer) -> None:
         cfg = trainer.cfg
         shape = (cfg.micro_batch * cfg.seq, cfg.hidden)
-        st = trainer.streams[self.rank]
+        st = trainer.streams[self.dev]
         self.post_recvs(lambda key: trainer.pool.get(shape, trainer.dtype, st), stream=st)
 
     def send_msg(self, trainer, key, tensor, src, dst) -> None:
@@ -187,8 +210,8 @@ class DistContext:
         st = trainer.opt_stream
         st.wait_event(ev)
         sp = trainer.stage_params[(dr, s)]
-        paired = self.allreduce_stage(s, sp.grad, stream=st)
-        trainer._adam((dr, s), [sp.grad], [sp.flat], st, grad_scale=0.5 if paired else 1.0)
+        copies = self.allreduce_stage(s, sp.grad, stream=st)
+        trainer._adam((dr, s), [sp.grad], [sp.flat], st, grad_scale=1.0 / copies)
 
     def end_iteration(self, trainer) -> None:
         if self.slots:

@@ -133,7 +133,7 @@ class Trainer:
         self.dist = dist_ctx
         self.device = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
         torch.cuda.set_device(self.device)
-        self.local_devices = list(range(self.D)) if dist_ctx is None else [dist_ctx.rank]
+        self.local_devices = list(range(self.D)) if dist_ctx is None else [dist_ctx.dev]
         self.record_timeline = record_timeline
         self.step_count = 0
 
@@ -187,7 +187,7 @@ class Trainer:
         if dist_ctx is None:
             self.order = issue_order(schedule)
         else:
-            d = dist_ctx.rank
+            d = dist_ctx.dev
             self.order = [(d, i, t) for i, t in enumerate(schedule.per_device[d])]
             dist_ctx.setup(self)
         self.iter_done = None

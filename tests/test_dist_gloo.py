@@ -25,7 +25,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, approach, N, out_q):
+def _worker(rank, world, port, approach, N, out_q, replicas=1):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -39,15 +39,18 @@ def _worker(rank, world, port, approach, N, out_q):
         cfg = CONFIGS["tiny"]
         oc = O.OracleConfig(cfg.layers, cfg.hidden, cfg.heads, cfg.seq, cfg.vocab, cfg.micro_batch, cfg.causal,
                             lr=1e-3)
-        sched = ps.build(ps.ApproachId(approach), world, N)
+        D = world // replicas
+        w, dev = divmod(rank, D)
+        sched = ps.build(ps.ApproachId(approach), D, N)
         S = sched.num_stages
         hbs = O.stage_halfblocks(cfg.layers, S)
         params = init_params(cfg, 7, perturb=True)
-        tok, tgt = synthetic_batch(cfg, N, seed=11)
+        tok, tgt = synthetic_batch(cfg, N * replicas, seed=11)   # replica w takes micro-batches [w N, (w+1) N)
+        tok, tgt = tok[w * N:(w + 1) * N], tgt[w * N:(w + 1) * N]
         dirs = list(sched.directions)
         n_rep = N // len(dirs)
         reps = {d: {k: v.double().clone().requires_grad_(True) for k, v in params.items()} for d in dirs}
-        ctx = DistContext(rank, world, cuda=False)
+        ctx = DistContext(rank, world, cuda=False, replicas=replicas)
         ctx.build_groups(sched)
         ctx.post_recvs(lambda key: torch.empty(cfg.micro_batch, cfg.seq, cfg.hidden, dtype=torch.float64))
         losses = {}
@@ -59,7 +62,7 @@ def _worker(rank, world, port, approach, N, out_q):
             out = O._run_stage(P, hbs[t.stage], x0, oc, first=t.stage == 0, last=t.stage == S - 1,
                                tokens=tok[t.micro_batch - 1], targets=tgt[t.micro_batch - 1])
             if t.stage == S - 1:
-                losses[t.micro_batch] = out.item()
+                losses[w * N + t.micro_batch] = out.item()
                 return (x0, out), None
             return (x0, out), out.detach()
 
@@ -88,7 +91,7 @@ def _worker(rank, world, port, approach, N, out_q):
             flat = torch.cat([P[n].grad.reshape(-1) for n in names])
             synced[(dr, s)] = (names, flat, ctx.allreduce_stage(s, flat))
 
-        order = [(rank, i, t) for i, t in enumerate(sched.per_device[rank])]
+        order = [(dev, i, t) for i, t in enumerate(sched.per_device[dev])]
         msgs, stashes = drive(order, S, sched.last_backward_positions(), forward=forward, backward=backward,
                               send=send, recv=recv, stage_done=stage_done,
                               dev_of=lambda dr, s: sched.stage_map(dr).device_of(s))
@@ -96,9 +99,8 @@ def _worker(rank, world, port, approach, N, out_q):
         ctx.finish_allreduces()
         assert not msgs and not stashes and not ctx.slots
         grads = {}
-        for (dr, s), (names, flat, paired) in synced.items():
-            if paired:
-                flat *= 0.5
+        for (dr, s), (names, flat, copies) in synced.items():
+            flat /= copies
             off = 0
             for n in names:
                 k = params[n].numel()
@@ -114,15 +116,20 @@ def O_stage_names(cfg, hbs, first, last):
     return stage_param_names(StagePlan(0, tuple(hbs), first, last))
 
 
-@pytest.mark.parametrize("approach,world,N", [("bitpipe", 2, 4), ("bitpipe", 4, 8), ("dapple-1f1b", 2, 4),
-                                              ("chimera", 4, 4), ("bitpipe-early-forward", 2, 4)])
-def test_distributed_host_logic_gloo(approach, world, N):
+@pytest.mark.parametrize("approach,world,N,replicas", [("bitpipe", 2, 4, 1), ("bitpipe", 4, 8, 1),
+                                                       ("dapple-1f1b", 2, 4, 1), ("chimera", 4, 4, 1),
+                                                       ("bitpipe-early-forward", 2, 4, 1),
+                                                       ("bitpipe", 4, 4, 2), ("dapple-1f1b", 4, 4, 2)])
+def test_distributed_host_logic_gloo(approach, world, N, replicas):
+    """world = replicas x D ranks; with replicas > 1 every pipeline replica
+    trains on its own N micro-batches and the stage groups span the replicas
+    (data parallelism, core.py:68 replicated_pipelines)."""
     from oracle import gpt_oracle as O
     from paper_2410_19367_b200.model import CONFIGS, init_params, synthetic_batch
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, approach, N, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, approach, N, q, replicas)) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=240) for _ in procs]
@@ -131,7 +138,7 @@ def test_distributed_host_logic_gloo(approach, world, N):
         assert p.exitcode == 0
     cfg = CONFIGS["tiny"]
     params = init_params(cfg, 7, perturb=True)
-    tok, tgt = synthetic_batch(cfg, N, seed=11)
+    tok, tgt = synthetic_batch(cfg, N * replicas, seed=11)
     oc = O.OracleConfig(cfg.layers, cfg.hidden, cfg.heads, cfg.seq, cfg.vocab, cfg.micro_batch, cfg.causal)
     seq = O.sequential_baseline(oc, params, tok, tgt)
     losses, grads = {}, {}
@@ -142,7 +149,7 @@ def test_distributed_host_logic_gloo(approach, world, N):
             if k in grads:   # both replicas of a stage hold the identical synced gradient
                 assert torch.equal(grads[k], v)
             grads[k] = v
-    assert sorted(losses) == list(range(1, N + 1))
+    assert sorted(losses) == list(range(1, N * replicas + 1))
     for m, v in losses.items():
         assert abs(v - seq.losses[m - 1].item()) < 1e-12
     assert set(grads) == set(params)
