@@ -48,10 +48,12 @@ def parse():
     ap.add_argument("--approach", default="bitpipe")
     ap.add_argument("--D", type=int, default=None)
     ap.add_argument("--N", type=int, default=16)
-    ap.add_argument("--order", default="paper", choices=["paper", "default"],
+    ap.add_argument("--order", default="paper", choices=["paper", "default", "search"],
                     help="BitPipe order: 'paper' = the F2 LayoutPolicy order (SURVEY §0 F2; bit-exact vs the "
                          "reference engine under that policy; reaches the analytic bubble) where one is known for "
-                         "D, else the reference default; 'default' = build_bitpipe's default policy")
+                         "D, else the policy search; 'search' = lowest-bubble reference-engine policy within "
+                         "--max-peak; 'default' = build_bitpipe's default policy")
+    ap.add_argument("--max-peak", type=float, default=None, help="activation cap (M_a per device) for --order search")
     ap.add_argument("--paper-policy", action="store_true", help="alias of --order paper")
     ap.add_argument("--replicas", type=int, default=1,
                     help="data-parallel pipeline replicas W (N>1 only): D = world / W, each replica on its own batch")
@@ -184,8 +186,12 @@ def main():
         D = args.D or 8
     N = args.N
     approach = ps.ApproachId.parse(args.approach)
-    use_paper = (args.order == "paper" or args.paper_policy) and D in ps.PAPER_GATE_STAGE
-    policy = ps.paper_policy(D) if use_paper and approach is ps.ApproachId.BITPIPE else None
+    policy = None
+    if approach is ps.ApproachId.BITPIPE and args.order != "default":
+        if (args.order == "paper" or args.paper_policy) and D in ps.PAPER_GATE_STAGE and args.max_peak is None:
+            policy = ps.paper_policy(D)
+        else:
+            policy = ps.search_bitpipe_policy(D, N, 2, max_peak=args.max_peak)[0]
     if approach in (ps.ApproachId.BITPIPE, ps.ApproachId.BITPIPE_EARLY_FORWARD):
         sched = ps.build_bitpipe(D, N, 2, approach is ps.ApproachId.BITPIPE_EARLY_FORWARD, policy=policy)
     else:
@@ -296,7 +302,7 @@ def main():
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform token ids, seed 1234; random-init "
                                                             "weights N(0,0.02))",
             "config": {"workload": f"{cfg.name} {approach.value} v=2 D={D} N={N}"
-                                   + (" (F2 paper policy)" if policy else "")
+                                   + (f" (layout policy gate {policy.gate_stage})" if policy else "")
                                    + (" all logical devices co-resident on 1 GPU" if G == 1 else ""),
                        "global_batch": W * N * cfg.micro_batch, "seq_len": cfg.seq, "layers": cfg.layers,
                        "hidden": cfg.hidden, "vocab": cfg.vocab, "parallelism": f"pp{D} bidirectional" + (f" x dp{W}" if W > 1 else ""),
@@ -321,7 +327,10 @@ def main():
                               "beta_ideal": beta_ideal, "model_tflops": value * F_tok / 1e12},
             "bubble": {"analytic": float(ps.analytic_bubble_ratio(approach, D, N)),
                        "canonical_of_order": beta_order,
-                       "order": "F2 paper policy" if policy else "reference default",
+                       "order": (f"layout policy defer={policy.defer} gate_stage={policy.gate_stage}"
+                                 + (" (F2 paper gate)" if ps.PAPER_GATE_STAGE.get(D) == policy.gate_stage
+                                    and not policy.defer else "")) if policy else "reference default",
+                       "peak_activations_Ma": float(max(ps.peak_activations(sched))),
                        "canonical_of_reference_default_order": beta_default_order,
                        "measured_replay": replay,
                        "note": "1 GPU: the D logical devices share the GPU, so pipeline bubbles are filled by other "

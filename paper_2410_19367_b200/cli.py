@@ -49,17 +49,25 @@ class UsageError(Exception):
 
 
 def build_one(approach: str, D: int, N: int, v: int | None = None, early_forward: bool = False,
-              order: str = "default") -> ps.Schedule:
+              order: str = "default", max_peak=None) -> ps.Schedule:
     """``build`` (builders.py:369-372) with the CLI's naming; ``order='paper'``
-    selects the F2 LayoutPolicy order for BitPipe when one is known for D."""
+    selects the F2 LayoutPolicy order for BitPipe when one is known for D,
+    ``order='search'`` the lowest-bubble policy of the reference engine within
+    an activation-peak cap (``search_bitpipe_policy``)."""
     try:
         a = ps.ApproachId.parse(approach)
     except Exception as exc:  # unknown approach name -> usage error
         raise UsageError(f"unknown approach {approach!r}") from exc
     if a is ps.ApproachId.BITPIPE and order == "paper":
         if D not in ps.PAPER_GATE_STAGE:
-            raise UsageError(f"no paper-policy order known for D={D} (known: {sorted(ps.PAPER_GATE_STAGE)})")
+            raise UsageError(f"no paper-policy order known for D={D} (known: {sorted(ps.PAPER_GATE_STAGE)}; "
+                             f"use --order search)")
         return ps.build_bitpipe(D, N, v or 2, early_forward, policy=ps.paper_policy(D))
+    if a is ps.ApproachId.BITPIPE and order == "search" and not early_forward:
+        try:
+            return ps.search_bitpipe_policy(D, N, v or 2, max_peak=max_peak)[1]
+        except ValueError as exc:
+            raise UsageError(str(exc)) from exc
     return ps.build(a, D, N, v, early_forward)
 
 
@@ -173,7 +181,7 @@ def _grid_points(args):
 def cmd_plan(args) -> int:
     for a in _approaches(args):
         for D, N in _grid_points(args):
-            s = build_one(a, D, N, args.v, args.early_forward, args.order)
+            s = build_one(a, D, N, args.v, args.early_forward, args.order, args.max_peak)
             name = f"{s.approach.value}_D{D}_N{N}" + ("_paper" if args.order == "paper" else "") + ".json"
             _emit(ps.dump_schedule(s), args.out, name)  # exact dump_schedule bytes
     return EXIT_OK
@@ -183,7 +191,7 @@ def _report_rows(args):
     rows = []
     for a in _approaches(args):
         for D, N in _grid_points(args):
-            s = build_one(a, D, N, args.v, args.early_forward, args.order)
+            s = build_one(a, D, N, args.v, args.early_forward, args.order, args.max_peak)
             dur, _ = _durations(s, args.model, args.partition)
             tl = timeline(s, dur)
             try:
@@ -217,7 +225,7 @@ def cmd_compare(args) -> int:
 def cmd_simulate(args) -> int:
     for a in _approaches(args):
         for D, N in _grid_points(args):
-            s = build_one(a, D, N, args.v, args.early_forward, args.order)
+            s = build_one(a, D, N, args.v, args.early_forward, args.order, args.max_peak)
             dur, note = _durations(s, args.model, args.partition)
             tl = timeline(s, dur)
             tl["durations"] = note
@@ -235,7 +243,7 @@ def cmd_search(args) -> int:
     (approach, D, N, order) point = N / makespan x D-normalised; the best
     row (lowest makespan per micro-batch per device) is repeated last."""
     rows = []
-    orders = ["default", "paper"] if args.order == "both" else [args.order]
+    orders = ["default", "paper", "search"] if args.order == "both" else [args.order]
     for order in orders:
         args_o = argparse.Namespace(**{**vars(args), "order": order})
         for r in _report_rows(args_o):
@@ -253,7 +261,7 @@ def cmd_search(args) -> int:
 def cmd_render(args) -> int:
     for a in _approaches(args):
         for D, N in _grid_points(args):
-            s = build_one(a, D, N, args.v, args.early_forward, args.order)
+            s = build_one(a, D, N, args.v, args.early_forward, args.order, args.max_peak)
             if args.format == "svg":
                 _emit(gantt_svg(timeline(s, s.canonical_duration)), args.out, f"{s.approach.value}_D{D}_N{N}.svg")
             else:
@@ -299,11 +307,12 @@ def cmd_verify(args) -> int:
     scheds = []
     for a in _approaches(args):
         for D, N in _grid_points(args):
-            s = build_one(a, D, N, args.v, args.early_forward, args.order)
+            s = build_one(a, D, N, args.v, args.early_forward, args.order, args.max_peak)
             scheds.append(s)
             fails = _verify_structure(s)
             # byte-determinism: an independent rebuild dumps the same bytes
-            if ps.dump_schedule(build_one(a, D, N, args.v, args.early_forward, args.order)) != ps.dump_schedule(s):
+            rebuilt = build_one(a, D, N, args.v, args.early_forward, args.order, args.max_peak)
+            if ps.dump_schedule(rebuilt) != ps.dump_schedule(s):
                 fails.append("rebuild is not byte-identical")
             failed += bool(fails)
             lines.append(f"{'FAIL' if fails else 'ok  '} structure {s.approach.value} D={D} N={N}"
@@ -372,7 +381,7 @@ def cmd_measure(args) -> int:
     cfg = CONFIGS[model]
     for a in _approaches(args):
         for D, N in _grid_points(args):
-            s = build_one(a, D, N, args.v, args.early_forward, args.order)
+            s = build_one(a, D, N, args.v, args.early_forward, args.order, args.max_peak)
             tr = Trainer(cfg, s, dtype=torch.bfloat16 if args.dtype == "bf16" else torch.float32,
                          optim=OptimConfig(), record_timeline=True, partition=args.partition)
             tok, tgt = synthetic_batch(cfg, N, seed=args.seed)
@@ -419,8 +428,11 @@ def make_parser() -> argparse.ArgumentParser:
         p.add_argument("--N", type=int, action="append", help="micro-batches (repeatable; default 2D)")
         p.add_argument("--v", type=int, default=None)
         p.add_argument("--early-forward", choices=["on", "off"], default="off")
-        p.add_argument("--order", choices=["default", "paper"] + (["both"] if name == "search" else []),
-                       default="default", help="BitPipe order policy (paper = SURVEY §0 F2)")
+        p.add_argument("--order", choices=["default", "paper", "search"] + (["both"] if name == "search" else []),
+                       default="default", help="BitPipe order policy (paper = SURVEY §0 F2 gate table; search = "
+                                               "lowest-bubble reference-engine policy within --max-peak)")
+        p.add_argument("--max-peak", type=float, default=None,
+                       help="activation cap for --order search, in M_a per device (PAPER Table 2: D)")
         p.add_argument("--model", default=None, help="cost model config (gpt-1.3b, bert-large, ...); "
                                                      "default canonical tf=1, tb=2")
         p.add_argument("--partition", choices=["uniform", "balanced"], default="uniform")

@@ -15,7 +15,7 @@ from .builders import (PAPER_GATE_STAGE, build, build_1f1b, build_bitpipe, build
                        build_gpipe, build_interleaved_looping, build_v_shaped,
                        merge_bidirectional, paper_policy)
 from .analysis import (analytic_bubble_ratio, analytic_makespan, canonical_bubble,
-                       canonical_replay)
+                       canonical_replay, peak_activations, search_bitpipe_policy)
 from . import errors
 
 __all__ = [
@@ -27,7 +27,7 @@ __all__ = [
     # extensions
     "BIDIRECTIONAL_APPROACHES", "dump_schedule", "load_schedule", "schedule_to_dict",
     "schedule_from_dict", "looping_map", "v_shaped_map", "FusedLayout", "LayoutPolicy",
-    "fused_layout", "list_schedule", "PAPER_GATE_STAGE", "paper_policy",
+    "fused_layout", "list_schedule", "PAPER_GATE_STAGE", "paper_policy", "peak_activations", "search_bitpipe_policy",
     "analytic_bubble_ratio", "analytic_makespan", "canonical_bubble", "canonical_replay",
     "errors",
 ]

@@ -101,3 +101,10 @@ def test_measure_timeline(capsys):
     tl = json.loads(out)
     assert rc == 0 and len(tl["tasks"]) == 4 * 4 * 8 and float(tl["makespan"]) > 0
     assert all(float(t["end"]) >= float(t["start"]) for t in tl["tasks"])
+
+
+def test_search_order_with_memory_cap(capsys):
+    rc, out, _ = run(capsys, "compare", "--approach", "bitpipe", "--D", "8", "--N", "16", "--order", "search",
+                     "--max-peak", "8", "--format", "json")
+    rows = json.loads(out)
+    assert rc == 0 and float(rows[0]["bubble_sim_float"]) < 0.2

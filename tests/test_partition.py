@@ -51,3 +51,27 @@ def test_device_loads_v_map_symmetry():
     ld = device_loads(cfg, [3] * 16, maps)
     assert all(abs(ld[d] - ld[7 - d]) < 1e-6 * ld[d] for d in range(8))
     assert ld[0] > ld[1]  # embedding + LM head stages sit on devices 0 and 7
+
+
+def test_policy_search_generalises_f2():
+    """Generalised F2: the policy search over the
+    reference engine's layout policies finds the analytic-bubble order at
+    D=8 N=16 (the F2 gate 10) and near-analytic orders where no gate is known
+    (D=6); with the PAPER Table 2 activation bound D M_a it still beats the
+    default order."""
+    pol, s, b, peak = ps.search_bitpipe_policy(8, 16)
+    assert b == ps.analytic_bubble_ratio(ps.ApproachId.BITPIPE, 8, 16) and pol.gate_stage == 10 and not pol.defer
+    assert peak == 12  # SURVEY §0 F2: 12 M_a at N=16
+    assert ps.dump_schedule(s) == ps.dump_schedule(ps.build_bitpipe(8, 16, policy=ps.paper_policy(8)))
+    _, s6, b6, _ = ps.search_bitpipe_policy(6, 12)
+    assert b6 < ps.canonical_bubble(ps.build_bitpipe(6, 12)) and b6 < Fraction(12, 100)
+    _, sc, bc, pc = ps.search_bitpipe_policy(8, 16, max_peak=8)
+    assert pc <= 8 and max(ps.peak_activations(sc)) <= 8
+    assert bc < ps.canonical_bubble(ps.build_bitpipe(8, 16))
+    with pytest.raises(ValueError):
+        ps.search_bitpipe_policy(4, 8, max_peak=1)
+
+
+def test_peak_activations_default_order():
+    """Non-EF BitPipe peaks lie in PAPER Table 2's [(D+3)/2, D] M_a (D=4 N=8 gives 3.5, 4, 4, 3.5)."""
+    assert ps.peak_activations(ps.build_bitpipe(4, 8)) == [Fraction(7, 2), 4, 4, Fraction(7, 2)]
