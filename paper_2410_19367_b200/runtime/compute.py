@@ -137,19 +137,38 @@ class StageCompute:
         l, half = divmod(self.plan.halfblocks[i], 2)
         return self.sp.g[f"layers.{l}." + ("attn.proj.b" if half == 0 else "mlp.fc2.b")]
 
-    def backward(self, stream, pool: BufferPool, st: Stash, dy, ws):
-        """Returns (dx0 or None, buffers to release after this task)."""
+    @staticmethod
+    def _wgrad(stream, wstream, fn):
+        """Issue a weight-gradient GEMM: on ``stream``, or (``wstream``) on the
+        side stream behind everything ``stream`` has issued so far, so it
+        overlaps the rest of the task's input-gradient chain (which carries
+        the pipeline's critical path to the previous stage)."""
+        if wstream is None:
+            fn(stream)
+            return
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        wstream.wait_event(ev)
+        fn(wstream)
+
+    def backward(self, stream, pool: BufferPool, st: Stash, dy, ws, wstream=None):
+        """Returns (dx0 or None, buffers to release after the task's ``stream``
+        work, buffers also read by side-stream weight-gradient GEMMs)."""
         cfg, P, G = self.cfg, self.sp.p, self.sp.g
         M, h, dt = self.M, cfg.hidden, self.dtype
         H, Dh = cfg.heads, cfg.head_dim
         scale = 1.0 / math.sqrt(Dh)
         release = st.buffers()
+        wread = []
+        wg = self._wgrad
         wb, self.wgrad_beta = self.wgrad_beta, 1.0
         if self.plan.head:
             xf, mean, rstd, dlogits = st.head
             dxf = pool.get((M, h), dt, stream)
             ops.gemm(dlogits, P["head.lm.w"], dxf, b_kmajor=False, stream=stream)
-            ops.gemm(dlogits, xf, G["head.lm.w"], a_kmajor=False, b_kmajor=False, beta=wb, stream=stream)
+            wg(stream, wstream, lambda q: ops.gemm(dlogits, xf, G["head.lm.w"], a_kmajor=False, b_kmajor=False,
+                                                   beta=wb, stream=q))
+            wread += [dlogits, xf]
             dy = pool.get((M, h), dt, stream)
             # the LN backward also sums its dx over rows: that is the output-bias
             # gradient of the half-block before it (fused, no separate launch)
@@ -169,7 +188,9 @@ class StageCompute:
             dx = pool.get((M, h), dt, stream)
             if half == 0:
                 _, a, mean, rstd, qkv, o, lse = save
-                ops.gemm(dy, o, G[p + "attn.proj.w"], a_kmajor=False, b_kmajor=False, beta=wb, stream=stream)
+                wg(stream, wstream, lambda q: ops.gemm(dy, o, G[p + "attn.proj.w"], a_kmajor=False, b_kmajor=False,
+                                                       beta=wb, stream=q))
+                wread += [dy, o]
                 if not bias_done:
                     ops.colsum_acc(dy, G[p + "attn.proj.b"], stream=stream)
                 do = pool.get((M, h), dt, stream)
@@ -179,7 +200,9 @@ class StageCompute:
                 # attention backward's epilogues
                 ops.attn_bwd(qkv, o, do, lse, dqkv, ws, cfg.micro_batch, cfg.seq, H, Dh, cfg.causal, scale,
                              stream=stream, dbias=G[p + "attn.qkv.b"])
-                ops.gemm(dqkv, a, G[p + "attn.qkv.w"], a_kmajor=False, b_kmajor=False, beta=wb, stream=stream)
+                wg(stream, wstream, lambda q: ops.gemm(dqkv, a, G[p + "attn.qkv.w"], a_kmajor=False,
+                                                       b_kmajor=False, beta=wb, stream=q))
+                wread += [dqkv, a]
                 da = pool.get((M, h), dt, stream)
                 ops.gemm(dqkv, P[p + "attn.qkv.w"], da, b_kmajor=False, stream=stream)
                 ops.layernorm_bwd(da, x, P[p + "ln1.w"], mean, rstd, dx, G[p + "ln1.w"], G[p + "ln1.b"], dres=dy,
@@ -187,7 +210,9 @@ class StageCompute:
                 release += [do, dqkv, da]
             else:
                 _, m, mean, rstd, u, g = save
-                ops.gemm(dy, g, G[p + "mlp.fc2.w"], a_kmajor=False, b_kmajor=False, beta=wb, stream=stream)
+                wg(stream, wstream, lambda q: ops.gemm(dy, g, G[p + "mlp.fc2.w"], a_kmajor=False, b_kmajor=False,
+                                                       beta=wb, stream=q))
+                wread += [dy, g]
                 if not bias_done:
                     ops.colsum_acc(dy, G[p + "mlp.fc2.b"], stream=stream)
                 du = pool.get((M, cfg.ffn), dt, stream)
@@ -195,7 +220,9 @@ class StageCompute:
                 # gradient) are reduced in the same GEMM epilogue
                 ops.gemm(dy, P[p + "mlp.fc2.w"], du, b_kmajor=False, aux=u, epilogue=EPI_DGELU, stream=stream,
                          colsum=G[p + "mlp.fc1.b"])
-                ops.gemm(du, m, G[p + "mlp.fc1.w"], a_kmajor=False, b_kmajor=False, beta=wb, stream=stream)
+                wg(stream, wstream, lambda q: ops.gemm(du, m, G[p + "mlp.fc1.w"], a_kmajor=False, b_kmajor=False,
+                                                       beta=wb, stream=q))
+                wread += [du, m]
                 dm = pool.get((M, h), dt, stream)
                 ops.gemm(du, P[p + "mlp.fc1.w"], dm, b_kmajor=False, stream=stream)
                 ops.layernorm_bwd(dm, x, P[p + "ln2.w"], mean, rstd, dx, G[p + "ln2.w"], G[p + "ln2.b"], dres=dy,
@@ -207,6 +234,11 @@ class StageCompute:
             dy = dx
         if self.plan.embed:
             ops.embed_bwd(st.tokens, dy, G["embed.wte"], G["embed.wpe"], cfg.micro_batch, cfg.seq, stream=stream)
-            return None, release
-        # dy is now the gradient w.r.t. the stage input: it becomes the message
-        return dy, [t for t in release if t is not dy]
+            dx0 = None
+        else:  # dy is now the gradient w.r.t. the stage input: it becomes the message
+            dx0 = dy
+            release = [t for t in release if t is not dy]
+        if wstream is None:
+            return dx0, release, []
+        wids = {id(t) for t in wread}
+        return dx0, [t for t in release if id(t) not in wids], [t for t in release if id(t) in wids]
