@@ -192,6 +192,12 @@ BP_API int bp_attn_bwd_ex(int dtype, int B, int S, int H, int Dh, int causal, fl
 BP_API int bp_adam(int64_t n, int param_dtype, float* master, const float* grad_a, const float* grad_b,
             float* m, float* v, void* param_a, void* param_b, float lr, float beta1, float beta2,
             float eps, float weight_decay, int step, float grad_scale, void* stream);
+/* as bp_adam with the step counter read on the device from *step_dev when
+ * step_dev is non-NULL (ABI 2; CUDA-graph replays of a train step advance it
+ * on the device). */
+BP_API int bp_adam_dev(int64_t n, int param_dtype, float* master, const float* grad_a, const float* grad_b,
+            float* m, float* v, void* param_a, void* param_b, float lr, float beta1, float beta2,
+            float eps, float weight_decay, int step, const int* step_dev, float grad_scale, void* stream);
 
 #ifdef __cplusplus
 }

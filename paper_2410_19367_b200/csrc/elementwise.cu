@@ -290,7 +290,12 @@ template <typename P>
 __global__ void adam_kernel(int64_t n, float* __restrict__ master, const float* __restrict__ ga,
                             const float* __restrict__ gb, float* __restrict__ m, float* __restrict__ v,
                             P* __restrict__ pa, P* __restrict__ pb, float lr, float b1, float b2, float eps, float wd,
-                            float bc1, float bc2, float gscale) {
+                            float bc1, float bc2, float gscale, const int* __restrict__ step_dev) {
+  if (step_dev) {  // step counter in device memory (CUDA-graph replays advance it on the device)
+    const float t = (float)*step_dev;
+    bc1 = 1.f - powf(b1, t);
+    bc2 = 1.f - powf(b2, t);
+  }
   const int64_t n4 = n / 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
@@ -438,10 +443,23 @@ extern "C" int bp_cast(int sd, int dd, int64_t n, const void* src, void* dst, vo
   return BP_OK;
 }
 
+extern "C" int bp_adam_dev(int64_t n, int param_dtype, float* master, const float* grad_a, const float* grad_b,
+                           float* m, float* v, void* param_a, void* param_b, float lr, float beta1, float beta2,
+                           float eps, float weight_decay, int step, const int* step_dev, float grad_scale,
+                           void* stream);
+
 extern "C" int bp_adam(int64_t n, int param_dtype, float* master, const float* grad_a, const float* grad_b, float* m,
                        float* v, void* param_a, void* param_b, float lr, float beta1, float beta2, float eps,
                        float weight_decay, int step, float grad_scale, void* stream) {
-  if (n <= 0 || step < 1) {
+  return bp_adam_dev(n, param_dtype, master, grad_a, grad_b, m, v, param_a, param_b, lr, beta1, beta2, eps,
+                     weight_decay, step, nullptr, grad_scale, stream);
+}
+
+extern "C" int bp_adam_dev(int64_t n, int param_dtype, float* master, const float* grad_a, const float* grad_b,
+                           float* m, float* v, void* param_a, void* param_b, float lr, float beta1, float beta2,
+                           float eps, float weight_decay, int step, const int* step_dev, float grad_scale,
+                           void* stream) {
+  if (n <= 0 || (step < 1 && !step_dev)) {
     set_error("adam: bad n/step");
     return BP_ERR_INVALID;
   }
@@ -451,15 +469,15 @@ extern "C" int bp_adam(int64_t n, int param_dtype, float* master, const float* g
     return BP_ERR_INVALID;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
+  const float bc1 = 1.f - powf(beta1, (float)(step < 1 ? 1 : step)), bc2 = 1.f - powf(beta2, (float)(step < 1 ? 1 : step));
   const int g = grid_for(n / 4 + 1, 256);
   if (param_dtype == BP_F32)
     adam_kernel<float><<<g, 256, 0, st>>>(n, master, grad_a, grad_b, m, v, (float*)param_a, (float*)param_b, lr, beta1,
-                                          beta2, eps, weight_decay, bc1, bc2, grad_scale);
+                                          beta2, eps, weight_decay, bc1, bc2, grad_scale, step_dev);
   else
     adam_kernel<__nv_bfloat16><<<g, 256, 0, st>>>(n, master, grad_a, grad_b, m, v, (__nv_bfloat16*)param_a,
                                                   (__nv_bfloat16*)param_b, lr, beta1, beta2, eps, weight_decay, bc1,
-                                                  bc2, grad_scale);
+                                                  bc2, grad_scale, step_dev);
   count_launch();
   BP_CHECK_LAUNCH("adam");
   return BP_OK;

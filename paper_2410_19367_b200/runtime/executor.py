@@ -202,6 +202,9 @@ class Trainer:
             dist_ctx.setup(self)
         self.iter_done = None
         self.timeline = None
+        self.step_dev = torch.zeros(1, dtype=torch.int32, device=self.device)  # AdamW step on the device
+        self._graph_state = None
+        self._graph = None
 
     # ----------------------------------------------------------------- helpers --
     def _stream_priorities(self, mode) -> dict:
@@ -242,17 +245,61 @@ class Trainer:
         ops.adam(owner.master, grads[0], grads[1] if len(grads) > 1 else None, owner.m, owner.v,
                  params_out[0], params_out[1] if len(params_out) > 1 else None,
                  lr=o.lr, beta1=o.beta1, beta2=o.beta2, eps=o.eps, weight_decay=o.weight_decay,
-                 step=self.step_count, grad_scale=grad_scale, stream=stream)
+                 step=self.step_count, grad_scale=grad_scale, stream=stream, step_dev=self.step_dev)
+
+    # ------------------------------------------------------------ CUDA graph --
+    def enable_graph(self) -> None:
+        """Replay the train step as one CUDA graph from the next call on
+        (co-resident mode): the next ``train_step`` captures one iteration --
+        every kernel, cross-stream event edge, eager AdamW -- and later calls
+        copy the inputs into the captured buffers and replay it.  The step
+        counter lives on the device (``bp_adam_dev``), the buffer pool is warm
+        (no allocation inside the capture), so a replay is exactly one more
+        eager iteration.  Call after at least one eager step."""
+        if self.dist is not None:
+            raise RuntimeError("CUDA-graph replay is for the co-resident executor (NCCL P2P is not captured)")
+        if self.record_timeline:
+            raise RuntimeError("disable record_timeline to capture the step")
+        self._graph_state = "capture"
+
+    def _graph_step(self, tokens, targets) -> StepOutput:
+        if self._graph_state == "capture":
+            self._g_tok = tokens.clone()
+            self._g_tgt = targets.clone()
+            torch.cuda.synchronize(self.device)
+            self.pool.forget_events()  # the device is idle: no wait on events recorded outside the capture
+            cap = torch.cuda.Stream(device=self.device)
+            self.iter_done = None  # no edge to work outside the graph
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cap):
+                self._step_body(self._g_tok, self._g_tgt)
+            self._graph, self._graph_state = g, "replay"
+            self.iter_done = None
+            torch.cuda.synchronize(self.device)
+            self.pool.forget_events()  # captured events must not be waited on outside the graph
+        else:
+            if tokens.data_ptr() != self._g_tok.data_ptr():
+                self._g_tok.copy_(tokens, non_blocking=True)
+                self._g_tgt.copy_(targets, non_blocking=True)
+        self.step_count += 1
+        self._graph.replay()
+        return StepOutput(self.losses, self.step_count)
 
     # --------------------------------------------------------------- train step --
     def train_step(self, tokens: torch.Tensor, targets: torch.Tensor) -> StepOutput:
         """tokens/targets: int32 device tensors [N, B, S] already on this GPU."""
+        if self._graph_state is not None:
+            return self._graph_step(tokens, targets)
         self.step_count += 1
+        return self._step_body(tokens, targets)
+
+    def _step_body(self, tokens, targets) -> StepOutput:
         main = torch.cuda.current_stream(self.device)
         start_ev = torch.cuda.Event()
         if self.iter_done is not None:
             main.wait_event(self.iter_done)
         self.losses.zero_()
+        self.step_dev.add_(1)
         start_ev.record(main)
         for st in self.streams.values():
             st.wait_event(start_ev)
@@ -310,7 +357,7 @@ class Trainer:
             self.dist.end_iteration(self)
         done = torch.cuda.Event()
         done.record(self.opt_stream)
-        for st in self.streams.values():
+        for st in list(self.streams.values()) + list(self.wstreams.values()):
             ev = torch.cuda.Event()
             ev.record(st)
             main.wait_event(ev)

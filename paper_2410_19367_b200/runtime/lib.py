@@ -62,6 +62,8 @@ _SIGS = {
     "bp_attn_bwd_ex": (_i32, [_i32, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "bp_adam": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _f32, _f32, _f32, _f32, _i32, _f32,
                        _vp]),
+    "bp_adam_dev": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _f32, _f32, _f32, _f32, _i32, _vp,
+                           _f32, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -172,8 +172,10 @@ def attn_bwd(qkv, o, dout, lse, dqkv, workspace, B, S, H, Dh, causal, scale, str
 
 
 def adam(master, grad_a, grad_b, m, v, param_a, param_b, *, lr, beta1, beta2, eps, weight_decay, step,
-         grad_scale=1.0, stream=None):
+         grad_scale=1.0, stream=None, step_dev=None):
+    """Fused replica-mean AdamW; ``step_dev`` (int32 device scalar) makes the
+    kernel read the step on the device (CUDA-graph capturable)."""
     pdt = _dt(param_a) if param_a is not None else BP_F32
-    check(lib().bp_adam(master.numel(), pdt, _p(master), _p(grad_a), _p(grad_b), _p(m), _p(v), _p(param_a),
-                        _p(param_b), float(lr), float(beta1), float(beta2), float(eps), float(weight_decay),
-                        int(step), float(grad_scale), _s(stream)), "bp_adam")
+    check(lib().bp_adam_dev(master.numel(), pdt, _p(master), _p(grad_a), _p(grad_b), _p(m), _p(v), _p(param_a),
+                            _p(param_b), float(lr), float(beta1), float(beta2), float(eps), float(weight_decay),
+                            int(step), _p(step_dev), float(grad_scale), _s(stream)), "bp_adam")

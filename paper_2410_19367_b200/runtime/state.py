@@ -122,3 +122,11 @@ class BufferPool:
         for t in tensors:
             if t is not None:
                 self.free[(tuple(t.shape), t.dtype)].append((t, event, sid))
+
+    def forget_events(self) -> None:
+        """Drop the release events of every free buffer (call only when the
+        device is idle, e.g. after capturing a CUDA graph whose events must
+        not be waited on outside it)."""
+        for lst in self.free.values():
+            for i, (t, _ev, sid) in enumerate(lst):
+                lst[i] = (t, None, sid)

@@ -136,3 +136,33 @@ def test_fp32_non_uniform_partition(label, partition):
     if partition == "balanced":
         from paper_2410_19367_b200.model import balanced_counts
         assert tr.partition == balanced_counts(CONFIGS["small"], tr.sched)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_cuda_graph_replay_equals_eager(dtype):
+    """A captured-and-replayed train step (Trainer.enable_graph) continues the
+    eager trajectory: same per-micro-batch losses and AdamW weights after
+    three steps (device-side step counter, warm buffer pool), with new input
+    tensors copied into the captured ones."""
+    from paper_2410_19367_b200.runtime.executor import Trainer
+    cfg = CONFIGS["tiny"]
+    sched = ps.build_bitpipe(4, 8)
+    opt = OptimConfig(lr=1e-3)
+    params = init_params(cfg, 7, perturb=True)
+    batches = [synthetic_batch(cfg, sched.N, seed=20 + i) for i in range(3)]
+    a = Trainer(cfg, sched, dtype=dtype, optim=opt, params=params)
+    b = Trainer(cfg, sched, dtype=dtype, optim=opt, params=params)
+    for i, (tok, tgt) in enumerate(batches):
+        la = a.train_step(tok.int().cuda(), tgt.int().cuda()).losses.clone()
+        if i == 1:
+            b.enable_graph()
+        lb = b.train_step(tok.int().cuda(), tgt.int().cuda()).losses.clone()
+        torch.cuda.synchronize()
+        assert rel(lb.cpu(), la.cpu()) < (1e-6 if dtype == torch.float32 else 1e-3), i
+    # weights, over the whole model: bias / LayerNorm gradients are atomically
+    # accumulated (run-to-run order noise), which AdamW's 1/sqrt(v) turns into
+    # sign-level differences on the smallest gradients of individual tensors
+    ma, mb = a.gather("master"), b.gather("master")
+    va = torch.cat([ma[k].reshape(-1) for k in sorted(ma)])
+    vb = torch.cat([mb[k].reshape(-1) for k in sorted(ma)])
+    assert rel(vb, va) < (1e-5 if dtype == torch.float32 else 1e-3)
