@@ -1,5 +1,6 @@
 """Schedule sweep on GPT-1.3B (BASELINE config 4): BitPipe vs 1F1B vs
-interleaved vs Chimera (+ BitPipe-EF, BitPipe F2 paper policy) at D=2/4/8,
+interleaved vs Chimera (+ BitPipe-EF, BitPipe F2 paper policy, BitPipe policy search within D M_a)
+at D=2/4/8,
 N=2D..4D.  For each: 1-GPU co-resident tokens/s, the canonical and analytic
 bubble, and the ASAP replay of the executed order with measured task times
 (projected makespan / bubble / tokens/s with one GPU per logical device).
@@ -21,6 +22,7 @@ ap.add_argument("--config", default="gpt-1.3b")
 ap.add_argument("--Ds", default="2,4,8")
 ap.add_argument("--mult", default="2,4")
 ap.add_argument("--steps", type=int, default=2)
+ap.add_argument("--partition", default="balanced", choices=["balanced", "uniform"])
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 M = cfg.micro_batch * cfg.seq
@@ -30,6 +32,7 @@ for D in map(int, args.Ds.split(",")):
         cands = [("bitpipe", lambda: ps.build_bitpipe(D, N)),
                  ("bitpipe-paper-policy", (lambda: ps.build_bitpipe(D, N, policy=ps.paper_policy(D)))
                   if D in ps.PAPER_GATE_STAGE else None),
+                 ("bitpipe-policy-search-cap-D", lambda: ps.search_bitpipe_policy(D, N, max_peak=D)[1]),
                  ("bitpipe-early-forward", (lambda: ps.build_bitpipe(D, N, early_forward=True)) if N >= 2 * D else None),
                  ("dapple-1f1b", lambda: ps.build_1f1b(D, N)),
                  ("interleaved-looping", lambda: ps.build_interleaved_looping(D, N, 2)),
@@ -38,7 +41,7 @@ for D in map(int, args.Ds.split(",")):
             if mk is None:
                 continue
             sched = mk()
-            tr = Trainer(cfg, sched, dtype=torch.bfloat16, optim=OptimConfig())
+            tr = Trainer(cfg, sched, dtype=torch.bfloat16, optim=OptimConfig(), partition=args.partition)
             tok, tgt = synthetic_batch(cfg, N)
             tok, tgt = tok.int().cuda(), tgt.int().cuda()
             tr.train_step(tok, tgt)
@@ -52,7 +55,8 @@ for D in map(int, args.Ds.split(",")):
             ms = e0.elapsed_time(e1) / args.steps
             rep = tr.replay_bubble(tr.measure_task_times())
             appr = sched.approach
-            line = {"approach": name, "D": D, "N": N, "v": sched.v,
+            line = {"approach": name, "D": D, "N": N, "v": sched.v, "partition": tr.partition,
+                    "peak_activations_Ma": float(max(ps.peak_activations(sched))),
                     "coresident_1gpu_tokens_per_s": N * M / (ms / 1e3), "ms_per_step_1gpu": ms,
                     "bubble_analytic": float(ps.analytic_bubble_ratio(appr, D, N, sched.v)),
                     "bubble_canonical_order": float(ps.canonical_bubble(sched)),
