@@ -44,21 +44,32 @@ class Stash:
     saves: list = field(default_factory=list)
     head: tuple | None = None
     tokens: torch.Tensor | None = None
+    head_persistent: bool = False  # head xf / logits live in the stage's per-iteration slots
 
     def buffers(self):
         out = list(self.xs)
         for s in self.saves:
             out.extend(s[1:])
         if self.head is not None:
-            out.extend(self.head)
+            out.extend(self.head[1:3] if self.head_persistent else self.head)
         return out
 
 
 class StageCompute:
     """Forward/backward of one stage replica with a fixed parameter store."""
 
-    def __init__(self, cfg: ModelConfig, plan: StagePlan, params: StageParams, *, grad_scale: float):
+    def __init__(self, cfg: ModelConfig, plan: StagePlan, params: StageParams, *, grad_scale: float,
+                 n_rep: int = 1):
         self.cfg, self.plan, self.sp = cfg, plan, params
+        # LM head weight gradient deferred to the replica's last backward of
+        # the iteration: one GEMM over all n_rep micro-batches (K = n_rep M)
+        # writes dW once instead of n_rep fp32 read-modify-write passes over
+        # the V x h gradient; the micro-batches' LN-f outputs and dlogits stay
+        # in per-iteration slots until then
+        self.n_rep = n_rep
+        self.defer_head_wgrad = plan.head and n_rep > 1
+        self._head_xf = self._head_logits = None
+        self._fwd_slot = self._bwd_count = 0
         self.dtype = params.dtype
         self.M = cfg.micro_batch * cfg.seq
         self.grad_scale = grad_scale          # d(step objective)/d(micro-batch mean loss)
@@ -77,6 +88,7 @@ class StageCompute:
         replaces zeroing the (large) GEMM-weight part of the gradient buffer.
         All backwards of one replica run on one stream, in issue order."""
         self.wgrad_beta = 0.0
+        self._fwd_slot = self._bwd_count = 0
 
     # ------------------------------------------------------------- forward --
     def forward(self, stream, pool: BufferPool, *, x0=None, tokens=None, targets=None, loss_slot=None):
@@ -116,10 +128,20 @@ class StageCompute:
             st.xs.append(y)
         if self.plan.head:
             x = st.xs[-1]
-            xf = pool.get((M, h), dt, stream)
+            if self.defer_head_wgrad:
+                if self._head_xf is None:
+                    self._head_xf = torch.empty(self.n_rep * M, h, dtype=dt, device=x.device)
+                    self._head_logits = torch.empty(self.n_rep * M, cfg.vocab, dtype=dt, device=x.device)
+                slot = self._fwd_slot % self.n_rep
+                self._fwd_slot += 1
+                xf = self._head_xf[slot * M:(slot + 1) * M]
+                logits = self._head_logits[slot * M:(slot + 1) * M]
+                st.head_persistent = True
+            else:
+                xf = pool.get((M, h), dt, stream)
+                logits = pool.get((M, cfg.vocab), dt, stream)
             mean, rstd = pool.get((M,), f32, stream), pool.get((M,), f32, stream)
             ops.layernorm_fwd(x, P["head.lnf.w"], P["head.lnf.b"], xf, mean, rstd, cfg.ln_eps, stream=stream)
-            logits = pool.get((M, cfg.vocab), dt, stream)
             ops.gemm(xf, P["head.lm.w"], logits, stream=stream)
             ops.xent_fwd_bwd(logits, targets, loss_slot, grad_scale=self.grad_scale * self.loss_scale,
                              loss_scale=self.loss_scale, stream=stream)
@@ -166,9 +188,15 @@ class StageCompute:
             xf, mean, rstd, dlogits = st.head
             dxf = pool.get((M, h), dt, stream)
             ops.gemm(dlogits, P["head.lm.w"], dxf, b_kmajor=False, stream=stream)
-            wg(stream, wstream, lambda q: ops.gemm(dlogits, xf, G["head.lm.w"], a_kmajor=False, b_kmajor=False,
-                                                   beta=wb, stream=q))
-            wread += [dlogits, xf]
+            if not self.defer_head_wgrad:
+                wg(stream, wstream, lambda q: ops.gemm(dlogits, xf, G["head.lm.w"], a_kmajor=False, b_kmajor=False,
+                                                       beta=wb, stream=q))
+                wread += [dlogits, xf]
+            else:
+                self._bwd_count += 1
+                if self._bwd_count == self.n_rep:  # all of the iteration's micro-batches are in the slots
+                    wg(stream, wstream, lambda q: ops.gemm(self._head_logits, self._head_xf, G["head.lm.w"],
+                                                           a_kmajor=False, b_kmajor=False, beta=0.0, stream=q))
             dy = pool.get((M, h), dt, stream)
             # the LN backward also sums its dx over rows: that is the output-bias
             # gradient of the half-block before it (fused, no separate launch)

@@ -153,7 +153,7 @@ class Trainer:
                 sp = StageParams(cfg, self.plans[s], dtype, self.device)
                 sp.load(params)
                 self.stage_params[(dr, s)] = sp
-                self.compute[(dr, s)] = StageCompute(cfg, self.plans[s], sp, grad_scale=grad_scale)
+                self.compute[(dr, s)] = StageCompute(cfg, self.plans[s], sp, grad_scale=grad_scale, n_rep=self.n_rep)
         if dist_ctx is None:  # all stages local: fuse each stage's last output-bias gradient
             for dr in self.dirs:  # into the next stage's message-producing LayerNorm backward
                 for s in range(1, self.S):
@@ -438,6 +438,11 @@ class Trainer:
         d0 = self.local_devices[0]
         out = {}
         torch.cuda.synchronize(dev)
+        # per-micro-batch LM-head weight gradient while timing tasks in
+        # isolation (the deferred one-GEMM form only exists at iteration level)
+        deferred = {k: c.defer_head_wgrad for k, c in self.compute.items()}
+        for c in self.compute.values():
+            c.defer_head_wgrad = False
         for (dr, s), comp in self.compute.items():
             ft, bt = [], []
             for _ in range(reps + 1):
@@ -460,6 +465,8 @@ class Trainer:
             out[(dr, s, "B")] = sorted(bt[1:])[len(bt[1:]) // 2]
         for sp in self.stage_params.values():
             sp.grad.zero_()
+        for k, c in self.compute.items():
+            c.defer_head_wgrad = deferred[k]
         return out
 
     def replay_bubble(self, times: dict) -> dict:
