@@ -108,7 +108,8 @@ class Trainer:
 
     def __init__(self, cfg: ModelConfig, schedule: Schedule, *, dtype=torch.bfloat16, optim: OptimConfig | None = None,
                  params: dict | None = None, seed: int = 1234, device=None, dist_ctx=None, record_timeline=False,
-                 serial_streams: bool = False, partition="uniform", stream_priority=None, wgrad_stream=None):
+                 serial_streams: bool = False, partition="uniform", stream_priority=None, wgrad_stream=None,
+                 defer_wgrad=None):
         if not torch.cuda.is_available():
             raise RuntimeError("BitPipe Trainer needs a CUDA device (no CPU fallback)")
         ops.lib()  # fail loudly now if the kernel library is missing
@@ -145,6 +146,9 @@ class Trainer:
         self.stage_params: dict = {}
         self.compute: dict = {}
         grad_scale = 1.0 / self.n_rep
+        if defer_wgrad is None:  # env BP_DEFER_WGRAD=0: per-micro-batch weight-gradient GEMMs (less memory)
+            import os
+            defer_wgrad = os.environ.get("BP_DEFER_WGRAD", "1") == "1"
         for dr in self.dirs:
             smap = schedule.stage_map(dr)
             for s in range(self.S):
@@ -153,7 +157,8 @@ class Trainer:
                 sp = StageParams(cfg, self.plans[s], dtype, self.device)
                 sp.load(params)
                 self.stage_params[(dr, s)] = sp
-                self.compute[(dr, s)] = StageCompute(cfg, self.plans[s], sp, grad_scale=grad_scale, n_rep=self.n_rep)
+                self.compute[(dr, s)] = StageCompute(cfg, self.plans[s], sp, grad_scale=grad_scale, n_rep=self.n_rep,
+                                                     defer_wgrad=defer_wgrad)
         if dist_ctx is None:  # all stages local: fuse each stage's last output-bias gradient
             for dr in self.dirs:  # into the next stage's message-producing LayerNorm backward
                 for s in range(1, self.S):
@@ -438,11 +443,11 @@ class Trainer:
         d0 = self.local_devices[0]
         out = {}
         torch.cuda.synchronize(dev)
-        # per-micro-batch LM-head weight gradient while timing tasks in
-        # isolation (the deferred one-GEMM form only exists at iteration level)
-        deferred = {k: c.defer_head_wgrad for k, c in self.compute.items()}
+        # per-micro-batch weight gradients while timing tasks in isolation
+        # (the deferred one-GEMM-per-weight form only exists at iteration level)
+        deferred = {k: c.defer_wgrad for k, c in self.compute.items()}
         for c in self.compute.values():
-            c.defer_head_wgrad = False
+            c.defer_wgrad = False
         for (dr, s), comp in self.compute.items():
             ft, bt = [], []
             for _ in range(reps + 1):
@@ -466,7 +471,7 @@ class Trainer:
         for sp in self.stage_params.values():
             sp.grad.zero_()
         for k, c in self.compute.items():
-            c.defer_head_wgrad = deferred[k]
+            c.defer_wgrad = deferred[k]
         return out
 
     def replay_bubble(self, times: dict) -> dict:
