@@ -146,9 +146,13 @@ class Trainer:
         self.stage_params: dict = {}
         self.compute: dict = {}
         grad_scale = 1.0 / self.n_rep
-        if defer_wgrad is None:  # env BP_DEFER_WGRAD=0: per-micro-batch weight-gradient GEMMs (less memory)
+        if defer_wgrad is None:  # env BP_DEFER_WGRAD=0/1 forces; default: on when the slots fit
             import os
-            defer_wgrad = os.environ.get("BP_DEFER_WGRAD", "1") == "1"
+            env = os.environ.get("BP_DEFER_WGRAD")
+            if env is not None:
+                defer_wgrad = env == "1"
+            else:
+                defer_wgrad = self._slot_bytes(dtype) <= 0.4 * torch.cuda.get_device_properties(self.device).total_memory
         for dr in self.dirs:
             smap = schedule.stage_map(dr)
             for s in range(self.S):
@@ -212,6 +216,26 @@ class Trainer:
         self._graph = None
 
     # ----------------------------------------------------------------- helpers --
+    def _slot_bytes(self, dtype) -> int:
+        """Device memory the deferred weight-gradient slots of this process's
+        stage replicas take: per half-block n_rep micro-batches of (attention)
+        a, o, dy, dqkv = 6h or (MLP) m, g, dy, du = 2h + 2 ffn columns, plus
+        LN-f output and logits on the head stage."""
+        cfg = self.cfg
+        esz = torch.empty(0, dtype=dtype).element_size()
+        rows = self.n_rep * cfg.micro_batch * cfg.seq
+        total = 0
+        for dr in self.dirs:
+            smap = self.sched.stage_map(dr)
+            for s in range(self.S):
+                if smap.device_of(s) not in self.local_devices:
+                    continue
+                for hb in self.plans[s].halfblocks:
+                    total += rows * (6 * cfg.hidden if hb % 2 == 0 else 2 * cfg.hidden + 2 * cfg.ffn) * esz
+                if self.plans[s].head:
+                    total += rows * (cfg.hidden + cfg.vocab) * esz
+        return total
+
     def _stream_priorities(self, mode) -> dict:
         """Co-resident CUDA stream priorities (lower = more urgent).  'tail':
         the logical devices whose lists finish last in the canonical replay
