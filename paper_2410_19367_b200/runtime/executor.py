@@ -158,8 +158,13 @@ class Trainer:
             for s in range(self.S):
                 if smap.device_of(s) not in self.local_devices:
                     continue
-                sp = StageParams(cfg, self.plans[s], dtype, self.device)
-                sp.load(params)
+                # co-resident: the second direction's replica reads the first's
+                # working weights (bit-identical by construction);
+                # AdamW then writes one bf16 copy per stage
+                other = self.stage_params.get((self.dirs[0], s)) if dist_ctx is None and dr != self.dirs[0] else None
+                sp = StageParams(cfg, self.plans[s], dtype, self.device, share_params=other)
+                if other is None:
+                    sp.load(params)
                 self.stage_params[(dr, s)] = sp
                 self.compute[(dr, s)] = StageCompute(cfg, self.plans[s], sp, grad_scale=grad_scale, n_rep=self.n_rep,
                                                      defer_wgrad=defer_wgrad)
@@ -428,7 +433,7 @@ class Trainer:
         for e in done_dirs[s].values():
             st.wait_event(e)
         grads = [self.stage_params[(x, s)].grad for x in self.dirs]
-        outs = [self.stage_params[(x, s)].flat for x in self.dirs]
+        outs = list({id(t): t for t in (self.stage_params[(x, s)].flat for x in self.dirs)}.values())  # shared: one
         self._adam(s, grads, outs, st)
 
     # ---------------------------------------------------------- introspection --

@@ -28,7 +28,10 @@ GEMM_WEIGHTS = ("attn.qkv.w", "attn.proj.w", "mlp.fc1.w", "mlp.fc2.w", "head.lm.
 class StageParams:
     """Flat storage of one stage replica's parameters and gradients."""
 
-    def __init__(self, cfg: ModelConfig, plan: StagePlan, dtype: torch.dtype, device):
+    def __init__(self, cfg: ModelConfig, plan: StagePlan, dtype: torch.dtype, device, share_params=None):
+        """``share_params``: another replica's StageParams of the same stage
+        whose working weights this replica uses (co-resident replicas are
+        bit-identical at every step; gradients stay separate)."""
         shapes = {n: s for n, s, _ in param_specs(cfg)}
         # GEMM-written weight gradients last: the first backward of an
         # iteration writes them (beta = 0) instead of accumulating, so only the
@@ -50,7 +53,8 @@ class StageParams:
             self.zero_numel = self.numel
         self.dtype = dtype
         self.device = torch.device(device)
-        self.flat = torch.zeros(self.numel, dtype=dtype, device=device)
+        self.flat = share_params.flat if share_params is not None else torch.zeros(self.numel, dtype=dtype,
+                                                                                    device=device)
         self.grad = torch.zeros(self.numel, dtype=torch.float32, device=device)
         self.shapes = {n: tuple(shapes[n]) for n in self.names}
         self.p = {n: self._view(self.flat, n) for n in self.names}
