@@ -345,8 +345,7 @@ def _verify_gpu(scheds, lines, args) -> int:
         tr = Trainer(cfg, s, dtype=torch.float32, optim=OptimConfig(lr=1e-3), params=params)
         out = tr.train_step(tok.int().cuda(), tgt.int().cuda())
         if s.is_bidirectional:
-            gd, gu = tr.gather("grads", ps.Direction.DOWN), tr.gather("grads", ps.Direction.UP)
-            grads = {k: 0.5 * (gd[k] + gu[k]) for k in gd}
+            grads = tr.mean_grads()
         else:
             grads = tr.gather("grads")
         rl, rg = refs[s.N]

@@ -78,6 +78,13 @@ class StageCompute:
         self.defer_wgrad = defer_wgrad and n_rep > 1
         self._slots: dict = {}
         self._fwd_slot = self._bwd_count = 0
+        # co-resident bidirectional pipelines: both replicas of a stage share
+        # one slot set ([slot_total * M] rows, this replica's micro-batches at
+        # rows slot_base * M ...) and the executor issues ONE deferred GEMM per
+        # weight over both (K = N M, ``combined_wgrad``): dW is written once
+        # per stage and AdamW reads a single gradient for the GEMM weights
+        self.slot_base, self.slot_total = 0, n_rep
+        self.combined_wgrad = False
         # cross-stage bias-gradient fusion (coresident executor): the output
         # gradient of this stage IS the dx of the next stage's last LayerNorm
         # backward, which accumulates its column sums into this stage's last
@@ -96,7 +103,7 @@ class StageCompute:
     def _slot_all(self, key, width):
         t = self._slots.get(key)
         if t is None:
-            t = torch.empty(self.n_rep * self.M, width, dtype=self.dtype, device=self.sp.flat.device)
+            t = torch.empty(self.slot_total * self.M, width, dtype=self.dtype, device=self.sp.flat.device)
             self._slots[key] = t
         return t
 
@@ -105,8 +112,8 @@ class StageCompute:
         the stash) or a pool buffer."""
         if not self.defer_wgrad:
             return pool.get((self.M, width), self.dtype, stream)
-        M = self.M
-        t = self._slot_all(key, width)[st.slot * M:(st.slot + 1) * M]
+        M, k = self.M, self.slot_base + st.slot
+        t = self._slot_all(key, width)[k * M:(k + 1) * M]
         st.pinned.add(id(t))
         return t
 
@@ -187,8 +194,9 @@ class StageCompute:
         fn(wstream)
 
     def _deferred_wgrads(self, q):
-        """All of the iteration's weight gradients of this replica, one GEMM
-        per weight over the n_rep micro-batch slots (beta = 0)."""
+        """All of the iteration's weight gradients of this replica (or, with
+        shared slots, of both co-resident replicas), one GEMM per weight over
+        the slot_total micro-batch slots (beta = 0)."""
         G, S = self.sp.g, self._slots
         for hb in self.plan.halfblocks:
             l, half = divmod(hb, 2)
@@ -305,7 +313,7 @@ class StageCompute:
             dy = dx
         if defer:
             self._bwd_count += 1
-            if self._bwd_count == self.n_rep:  # every micro-batch of the iteration is in the slots
+            if self._bwd_count == self.n_rep and not self.combined_wgrad:  # every micro-batch is in the slots
                 wg(stream, wstream, self._deferred_wgrads)
         if self.plan.embed:
             ops.embed_bwd(st.tokens, dy, G["embed.wte"], G["embed.wpe"], cfg.micro_batch, cfg.seq, stream=stream)

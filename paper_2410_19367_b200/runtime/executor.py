@@ -38,7 +38,7 @@ from ..model import CONFIGS, ModelConfig, OptimConfig, balanced_counts, stage_pa
 from ..schedule import Direction, Schedule, TaskKind, canonical_replay
 from . import ops
 from .compute import StageCompute
-from .state import BufferPool, StageParams
+from .state import GEMM_WEIGHTS, BufferPool, StageParams
 
 __all__ = ["Trainer", "StepOutput", "issue_order", "drive"]
 
@@ -168,6 +168,17 @@ class Trainer:
                 self.stage_params[(dr, s)] = sp
                 self.compute[(dr, s)] = StageCompute(cfg, self.plans[s], sp, grad_scale=grad_scale, n_rep=self.n_rep,
                                                      defer_wgrad=defer_wgrad)
+        # co-resident bidirectional: one deferred weight-gradient GEMM per
+        # weight over both replicas' micro-batches (shared slots, K = N M),
+        # issued on the optimizer stream when both replicas are done
+        self.combined_wgrad = dist_ctx is None and self.bidir and defer_wgrad and self.n_rep > 1
+        if self.combined_wgrad:
+            for s in range(self.S):
+                c0, c1 = self.compute[(self.dirs[0], s)], self.compute[(self.dirs[1], s)]
+                c1._slots = c0._slots
+                c0.slot_total = c1.slot_total = 2 * self.n_rep
+                c1.slot_base = self.n_rep
+                c0.combined_wgrad = c1.combined_wgrad = True
         if dist_ctx is None:  # all stages local: fuse each stage's last output-bias gradient
             for dr in self.dirs:  # into the next stage's message-producing LayerNorm backward
                 for s in range(1, self.S):
@@ -273,10 +284,11 @@ class Trainer:
         for comp in self.compute.values():
             comp.begin_iteration()
 
-    def _adam(self, stage_key, grads, params_out, stream, grad_scale=1.0):
+    def _adam(self, stage_key, grads, params_out, stream, grad_scale=1.0, sl=None):
         owner = self.opt_owner[stage_key]
         o = self.optim
-        ops.adam(owner.master, grads[0], grads[1] if len(grads) > 1 else None, owner.m, owner.v,
+        a, b = sl if sl is not None else (0, owner.master.numel())
+        ops.adam(owner.master[a:b], grads[0], grads[1] if len(grads) > 1 else None, owner.m[a:b], owner.v[a:b],
                  params_out[0], params_out[1] if len(params_out) > 1 else None,
                  lr=o.lr, beta1=o.beta1, beta2=o.beta2, eps=o.eps, weight_decay=o.weight_decay,
                  step=self.step_count, grad_scale=grad_scale, stream=stream, step_dev=self.step_dev)
@@ -434,7 +446,30 @@ class Trainer:
             st.wait_event(e)
         grads = [self.stage_params[(x, s)].grad for x in self.dirs]
         outs = list({id(t): t for t in (self.stage_params[(x, s)].flat for x in self.dirs)}.values())  # shared: one
-        self._adam(s, grads, outs, st)
+        if not self.combined_wgrad:
+            self._adam(s, grads, outs, st)
+            return
+        # both replicas' GEMM-weight gradients in one set of GEMMs into the
+        # first replica's buffer (sum over N micro-batches); AdamW in two
+        # parts: the atomically accumulated head averages the two replicas,
+        # the GEMM-weight tail reads the combined sum at scale 1/2
+        sp0 = self.stage_params[(self.dirs[0], s)]
+        self.compute[(self.dirs[0], s)]._deferred_wgrads(st)
+        z = sp0.zero_numel
+        if z:
+            self._adam(s, [g[:z] for g in grads], [o[:z] for o in outs], st, sl=(0, z))
+        if z < sp0.numel:
+            self._adam(s, [grads[0][z:]], [o[z:] for o in outs], st, grad_scale=0.5, sl=(z, sp0.numel))
+
+    def mean_grads(self) -> dict:
+        """{name: fp32 CPU tensor}: the replica-mean gradient AdamW applies
+        (tests; synchronises).  Combined deferred weight gradients hold the
+        sum over both replicas in the first replica's buffer."""
+        if len(self.dirs) == 1:
+            return self.gather("grads")
+        gd, gu = self.gather("grads", self.dirs[0]), self.gather("grads", self.dirs[1])
+        return {k: 0.5 * gd[k] if (self.combined_wgrad and k.endswith(GEMM_WEIGHTS)) else 0.5 * (gd[k] + gu[k])
+                for k in gd}
 
     # ---------------------------------------------------------- introspection --
     def gather(self, what: str = "params", direction: Direction | None = None) -> dict:

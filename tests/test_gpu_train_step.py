@@ -74,9 +74,7 @@ def run_pair(label, text, cfg_name, dtype, tol_loss, tol_grad, check_params, par
     assert rel(losses, ref.losses) < tol_loss, (losses, ref.losses)
     # replica-mean gradients: our per-replica grads are pre-mean; average them
     if sched.is_bidirectional:
-        gd = tr.gather("grads", ps.Direction.DOWN)
-        gu = tr.gather("grads", ps.Direction.UP)
-        grads = {k: 0.5 * (gd[k] + gu[k]) for k in gd}
+        grads = tr.mean_grads()
     errs = {k: rel(grads[k], ref.grads[k]) for k in ref.grads}
     wk = max(errs, key=errs.get)
     assert errs[wk] < tol_grad, (wk, errs[wk], ref.grads[wk].norm().item())
