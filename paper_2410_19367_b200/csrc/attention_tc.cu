@@ -148,9 +148,14 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
   uint64_t* v_empty = v_full + 2;         // [2]
   uint64_t* s_full = v_full + 4;          // [2]
   uint64_t* s_free = v_full + 6;          // [2]
-  uint64_t* p_full = v_full + 8;
-  uint64_t* pv_done = v_full + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_full + 10);
+  // P(j) ready: one barrier per j mod 4.  S(j+1) is issued before P V(j), so
+  // a softmax warp can run up to two tiles ahead of a slower one (S(j+2)
+  // only waits for every warp to have READ S(j)); with a single barrier its
+  // arrival for tile j+1 would complete tile j's phase early
+  uint64_t* p_full = v_full + 8;   // [4]
+  uint64_t* pv_done = v_full + 12;
+  uint64_t* o_done = v_full + 13;  // single phase: every P V of the CTA complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_full + 14);
   // TMEM: S buffers [0,128) and [128,256) (P of tile j is written back as bf16
   // over the first 64 columns of its S buffer: the TMEM A operand of O += P V),
   // O [256, 256+Dh)
@@ -174,8 +179,9 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], 256);
     }
-    mbar_init(p_full, 256);
+    for (int i = 0; i < 4; ++i) mbar_init(&p_full[i], 256);
     mbar_init(pv_done, 1);
+    mbar_init(o_done, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -239,7 +245,7 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
         }
         if (j >= 1) {
           const int jj = j - 1, st = jj & 1;
-          mbar_wait(p_full, jj & 1);
+          mbar_wait(&p_full[jj & 3], (jj >> 2) & 1);
           mbar_wait(&v_full[st], (jj >> 1) & 1);
           TRACE_MMA(32 + jj, 9);
           tc_fence_after();
@@ -249,6 +255,7 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
             tc_mma_f16_ts(tmem + 256, tmem + st * 128 + 8 * ks, mndesc(aV, ks, 128), idesc_o, (jj > 0 || ks > 0));
           tc_commit(pv_done);
           tc_commit(&v_empty[st]);
+          if (jj == n_kv - 1) tc_commit(o_done);
         }
       }
     }
@@ -292,24 +299,27 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       named_bar_sync(1 + wq, 64);
       mx = fmaxf(mx, xs[(hh ^ 1) * 128 + r]);
       TRACE(32 + j, 3);
-      if (mx > m_used + 8.f) {
-        if (j > 0) {  // rescale O: needs P V of tile j-1 complete
-          mbar_wait(pv_done, (j - 1) & 1);
-          tc_fence_after();
-          const float f = ex2(m_used - mx);
+      // lazy rescale (only when a row max grew by > 2^8).  The decision is
+      // per row but tcgen05.ld / st are .sync.aligned warp collectives: the
+      // whole warp rescales when any of its rows needs it (f = 1 for the
+      // others) -- a partial-warp tcgen05.ld hangs the CTA
+      const bool up = mx > m_used + 8.f;
+      if (j > 0 && __any_sync(0xffffffffu, up)) {  // rescale O: needs P V of tile j-1 complete
+        mbar_wait(pv_done, (j - 1) & 1);
+        tc_fence_after();
+        const float f = up ? ex2(m_used - mx) : 1.f;
 #pragma unroll 1
-          for (int c = 0; c < OC; ++c) {
-            float ov[32];
-            const uint32_t ta = tl + 256 + (hh * OC + c) * 32;
-            tmem_ld_32x32b_x32(ta, ov);
+        for (int c = 0; c < OC; ++c) {
+          float ov[32];
+          const uint32_t ta = tl + 256 + (hh * OC + c) * 32;
+          tmem_ld_32x32b_x32(ta, ov);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] *= f;
-            tmem_st_32x32b_x32(ta, ov);
-          }
-          l *= f;
+          for (int i = 0; i < 32; ++i) ov[i] *= f;
+          tmem_st_32x32b_x32(ta, ov);
         }
-        m_used = mx;
+        l *= f;
       }
+      if (up) m_used = mx;
       TRACE(32 + j, 4);
       float l8[8];
 #pragma unroll
@@ -331,7 +341,7 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       TRACE(32 + j, 6);
       tmem_st_32x32b_x32(tl + st * 128 + hh * 32, pk);
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[j & 3]);
       TRACE(32 + j, 7);
     }
     // epilogue: O / l (l = sum of both halves' partial sums)
@@ -339,7 +349,9 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
     xs[hh * 128 + r] = l;
     named_bar_sync(1 + wq, 64);
     l += xs[(hh ^ 1) * 128 + r];
-    mbar_wait(pv_done, (n_kv - 1) & 1);
+    // not a parity wait on pv_done: that is ambiguous while P V(n_kv-2) may
+    // still be in flight (the last S commit only covers P V(n_kv-3))
+    mbar_wait(o_done, 0);
     tc_fence_after();
     const int q = qt * 128 + r;
     const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -534,21 +546,20 @@ fwd2_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__
                              fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
       if (threadIdx.x == 96) TRACE_MMA(32 + j, 2);
       const float mxs = mx * scale_log2;
-      if (mxs > m_used + 8.f) {
-        if (j > 0) {  // O_X holds PV(j-1) complete: S_X(j) was issued after it
-          const float f = ex2(m_used - mxs);
+      const bool up = mxs > m_used + 8.f;  // warp-uniform rescale (see fwd_tc)
+      if (j > 0 && __any_sync(0xffffffffu, up)) {  // O_X holds PV(j-1) complete: S_X(j) was issued after it
+        const float f = up ? ex2(m_used - mxs) : 1.f;
 #pragma unroll 1
-          for (int c = 0; c < Dh / 32; ++c) {
-            float ov[32];
-            tmem_ld_32x32b_x32(tO + c * 32, ov);
+        for (int c = 0; c < Dh / 32; ++c) {
+          float ov[32];
+          tmem_ld_32x32b_x32(tO + c * 32, ov);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] *= f;
-            tmem_st_32x32b_x32(tO + c * 32, ov);
-          }
-          l *= f;
+          for (int i = 0; i < 32; ++i) ov[i] *= f;
+          tmem_st_32x32b_x32(tO + c * 32, ov);
         }
-        m_used = mxs;
+        l *= f;
       }
+      if (up) m_used = mxs;
       if (threadIdx.x == 96) TRACE_MMA(32 + j, 3);
       float l8[8];
 #pragma unroll

@@ -205,6 +205,12 @@ class Trainer:
             self.streams = {d: torch.cuda.Stream(device=self.device, priority=prio.get(d, 0))
                             for d in self.local_devices}
         self.opt_stream = torch.cuda.Stream(device=self.device)
+        # co-resident: per-stage optimizer work (combined weight-gradient GEMMs
+        # + AdamW) round-robin over BP_OPT_STREAMS streams so the stages that
+        # finish together in the drain overlap (1 = one serial stream)
+        import os
+        nopt = max(1, int(os.environ.get("BP_OPT_STREAMS", "1")))
+        self.opt_streams = [self.opt_stream] + [torch.cuda.Stream(device=self.device) for _ in range(nopt - 1)]
         # weight-gradient GEMMs on a side stream per logical device, off the
         # critical path of the backward chain (the message to the previous
         # stage no longer waits for them; +0.5 % co-resident, more concurrency
@@ -349,7 +355,8 @@ class Trainer:
         start_ev.record(main)
         for st in self.streams.values():
             st.wait_event(start_ev)
-        self.opt_stream.wait_event(start_ev)
+        for st in self.opt_streams:
+            st.wait_event(start_ev)
         self._zero_grads()
         if self.dist is not None:
             self.dist.begin_iteration(self)
@@ -403,7 +410,7 @@ class Trainer:
             self.dist.end_iteration(self)
         done = torch.cuda.Event()
         done.record(self.opt_stream)
-        for st in list(self.streams.values()) + list(self.wstreams.values()):
+        for st in list(self.streams.values()) + list(self.wstreams.values()) + self.opt_streams[1:]:
             ev = torch.cuda.Event()
             ev.record(st)
             main.wait_event(ev)
@@ -441,7 +448,7 @@ class Trainer:
         done_dirs.setdefault(s, {})[dr] = ev
         if len(done_dirs[s]) < len(self.dirs):
             return
-        st = self.opt_stream
+        st = self.opt_streams[s % len(self.opt_streams)]
         for e in done_dirs[s].values():
             st.wait_event(e)
         grads = [self.stage_params[(x, s)].grad for x in self.dirs]

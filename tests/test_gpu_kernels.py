@@ -320,6 +320,37 @@ def _check_attention(dtype, B, S, H, Dh, causal):
     assert _relerr(dbias, 1 + dqkv.float().sum(0)) < 1e-5
 
 
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("fwd_mode", [1, 2], ids=["fwd-1tile", "fwd-2tile"])
+def test_attention_partial_warp_rescale(causal, fwd_mode):
+    """Rows whose running max jumps by > 2^8 at every key tile (even rows)
+    next to rows whose max never moves (odd rows): the forward kernels'
+    lazy O rescale is then wanted by half the lanes of each warp.  tcgen05.ld
+    / st are warp collectives, so a per-lane rescale branch hung the CTA
+    (intermittently, as soon as a warp diverged)."""
+    from paper_2410_19367_b200.runtime.lib import OPT_ATTN_FWD_MODE
+    B, S, H, Dh = 1, 1024, 2, 128
+    scale = 1.0 / math.sqrt(Dh)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    qkv = (torch.randn(B * S, 3, H, Dh, device="cuda", generator=g) * 0.05)
+    tile = torch.arange(S, device="cuda") // 128 + 1
+    qkv[:, 1, :, 0] += (10.0 * tile)[:, None]          # key tile j scores 80 (j + 1) with an even row
+    qkv[0::2, 0, :, 0] += 8.0
+    qkv[1::2, 0, :, 0] -= 8.0                           # odd rows: max stays at the first key tile
+    qkv = qkv.reshape(B * S, 3 * H * Dh).bfloat16()
+    o = torch.empty(B * S, H * Dh, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(B * H * S, device="cuda")
+    ops.set_option(OPT_ATTN_FWD_MODE, fwd_mode)
+    try:
+        ops.attn_fwd(qkv, o, lse, B, S, H, Dh, causal, scale)
+        torch.cuda.synchronize()
+    finally:
+        ops.set_option(OPT_ATTN_FWD_MODE, 0)
+    oref, lref = _attn_ref(qkv.float(), B, S, H, Dh, causal, scale)
+    assert _relerr(o.float(), oref) < 2e-2
+    assert _relerr(lse, lref) < 1e-3
+
+
 def test_adam_matches_torch():
     n = 1000003
     p = torch.randn(n, device="cuda")
