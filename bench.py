@@ -288,6 +288,7 @@ def main():
     if world == 1:
         tr.streams = {d: main_stream for d in tr.streams}
         tr.wstreams = {}  # weight-gradient GEMMs serialised too (their spans would include cross-stream waits)
+        tr.opt_stream, tr.opt_streams = main_stream, [main_stream]  # and the combined ones + AdamW
     tr.train_step(tok_d, tgt_d)
     torch.cuda.synchronize()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
