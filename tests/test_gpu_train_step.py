@@ -48,7 +48,8 @@ def rel(a, b):
     return ((a - b).norm() / b.norm().clamp_min(1e-30)).item()
 
 
-def run_pair(label, text, cfg_name, dtype, tol_loss, tol_grad, check_params, partition="uniform"):
+def run_pair(label, text, cfg_name, dtype, tol_loss, tol_grad, check_params, partition="uniform", defer_wgrad=None,
+             expect_combined=None):
     from paper_2410_19367_b200.runtime.executor import Trainer
     cfg = CONFIGS[cfg_name]
     sched = build_ours(label)
@@ -56,7 +57,10 @@ def run_pair(label, text, cfg_name, dtype, tol_loss, tol_grad, check_params, par
     opt = OptimConfig(lr=1e-3, weight_decay=0.01)
     params = init_params(cfg, 7, perturb=True)
     tok, tgt = synthetic_batch(cfg, sched.N, seed=11)
-    tr = Trainer(cfg, sched, dtype=dtype, optim=opt, params=params, record_timeline=True, partition=partition)
+    tr = Trainer(cfg, sched, dtype=dtype, optim=opt, params=params, record_timeline=True, partition=partition,
+                 defer_wgrad=defer_wgrad)
+    if expect_combined is not None:
+        assert tr.combined_wgrad == expect_combined
     # executed per-device order == schedule order, bit for bit
     issued = {}
     for d, i, t in tr.order:
@@ -134,6 +138,22 @@ def test_fp32_non_uniform_partition(label, partition):
     if partition == "balanced":
         from paper_2410_19367_b200.model import balanced_counts
         assert tr.partition == balanced_counts(CONFIGS["small"], tr.sched)
+
+
+@pytest.mark.parametrize("label", ["D=4;N=8;approach=bitpipe;v=2", "D=4;N=4;approach=chimera",
+                                   "D=4;N=4;approach=dapple-1f1b"])
+@pytest.mark.parametrize("defer", [False, True], ids=["per-microbatch-wgrad", "deferred-wgrad"])
+def test_fp32_weight_gradient_placement(label, defer):
+    """Per-micro-batch weight-gradient GEMMs, and deferred ones (one GEMM per
+    weight over the iteration's slots; co-resident bidirectional schedules:
+    ONE over both replicas' micro-batches, combined into the down replica's
+    gradient, split AdamW) give the oracle's losses, gradients and update."""
+    text = golden()[label] if label in golden() else None
+    if text is None:
+        pytest.skip("no golden dump for " + label)
+    bidir = "bitpipe" in label or "chimera" in label
+    run_pair(label, text, "tiny", torch.float32, 1e-4, 1e-4, 1e-3, defer_wgrad=defer,
+             expect_combined=defer and bidir)
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
