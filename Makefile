@@ -15,12 +15,12 @@ build/%.cu.o: $(PKG)/csrc/%.cu $(PKG)/csrc/*.cuh include/bitpipe.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-build/%.cpp.o: $(PKG)/csrc/%.cpp include/bitpipe.h
+build/%.cpp.o: $(PKG)/csrc/%.cpp include/bitpipe.h include/bitpipe_comm.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(LIB): $(OBJ)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -cudart static
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -cudart static -ldl
 
 clean:
 	rm -rf build $(LIB)

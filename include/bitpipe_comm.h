@@ -1,0 +1,94 @@
+/*
+ * bitpipe_comm.h -- C ABI of the BitPipe runtime context (part of
+ * libbitpipe_b200.so): the communicator, message-slot, event and CUDA-graph
+ * entry points of SURVEY §8(b)'s "minimal C exports", for hosts that drive
+ * the pipeline without torch.distributed (a C++ or FFI host).
+ *
+ * The reference has no FFI (pure-Python API); what these
+ * replace is the SPEC's train-step plumbing:
+ *   bp_init / bp_comm_split   -> the per-link and replica-pair groups of the
+ *                                executor (runtime/distributed.py)
+ *   bp_send / bp_recv         -> "activations/gradients flow along schedule
+ *                                edges", one message =
+ *                                message_size bytes (core.py:150-157)
+ *   bp_allreduce_mean         -> the eager replica-pair gradient mean after a
+ *                                stage's last backward
+ *   bp_graph_*                -> CUDA-graph capture / replay of a step
+ * The in-tree Python executor makes the same calls through torch.distributed
+ * (NCCL) and torch.cuda.CUDAGraph; both paths use the same NCCL library
+ * (loaded with dlopen("libnccl.so.2"), so a process that already loaded
+ * torch's NCCL shares it).
+ *
+ * Conventions as in bitpipe.h: device pointers owned by the caller, streams
+ * as void*, int status (BP_OK / BP_ERR_*) with bp_last_error().  NCCL
+ * failures return BP_ERR_COMM with the NCCL error string.  A bp_ctx owns
+ * its communicator and the slot slabs allocated through it; bp_destroy
+ * frees both (never caller memory).
+ */
+#ifndef BITPIPE_B200_COMM_H
+#define BITPIPE_B200_COMM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "bitpipe.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BP_ERR_COMM 4
+#define BP_NCCL_ID_BYTES 128
+
+typedef struct bp_ctx bp_ctx;
+
+/* 1 if an NCCL library could be loaded (no device work). */
+BP_API int bp_comm_available(void);
+/* A fresh NCCL unique id (rank 0 creates it, the host broadcasts the 128
+ * bytes to every rank out of band). */
+BP_API int bp_nccl_unique_id(void* id_out);
+/* One communicator over `world` ranks on CUDA `device` (collective: every
+ * rank calls it with the same id). */
+BP_API int bp_init(int rank, int world, const void* nccl_id, int device, bp_ctx** ctx_out);
+/* Sub-communicator of the ranks passing the same `color`, ordered by `key`
+ * (collective over ctx): directed P2P links, replica-pair stage groups.
+ * color < 0: this rank joins none (*ctx_out = NULL). */
+BP_API int bp_comm_split(bp_ctx* ctx, int color, int key, bp_ctx** ctx_out);
+BP_API int bp_comm_rank(const bp_ctx* ctx);
+BP_API int bp_comm_size(const bp_ctx* ctx);
+/* Message slots: `count` device buffers of `bytes` each, one slab owned by
+ * ctx (freed by bp_destroy); *base_out = first slot, slot i at base + i*bytes
+ * rounded up to 256 B (bp_slot_stride). */
+BP_API int bp_slots_alloc(bp_ctx* ctx, size_t bytes, int count, void** base_out);
+BP_API size_t bp_slot_stride(size_t bytes);
+/* Point-to-point messages (asynchronous on `stream`).  The receiver posts
+ * its receives from a peer in the order the peer sends them. */
+BP_API int bp_send(bp_ctx* ctx, int peer, const void* ptr, size_t bytes, void* stream);
+BP_API int bp_recv(bp_ctx* ctx, int peer, void* ptr, size_t bytes, void* stream);
+/* Bracket several bp_send / bp_recv into one fused NCCL group. */
+BP_API int bp_group_start(void);
+BP_API int bp_group_end(void);
+/* In-place mean over the communicator's ranks of n elements (BP_F32 or
+ * BP_BF16), asynchronous on `stream`. */
+BP_API int bp_allreduce_mean(bp_ctx* ctx, void* ptr, size_t n, int dtype, void* stream);
+/* Destroys the communicator and frees the ctx's slot slabs (sub-contexts
+ * are destroyed separately). */
+BP_API int bp_destroy(bp_ctx* ctx);
+
+/* Events (cudaEventDisableTiming) for cross-stream ordering. */
+BP_API int bp_event_create(void** ev_out);
+BP_API int bp_event_record(void* ev, void* stream);
+BP_API int bp_stream_wait_event(void* stream, void* ev);
+BP_API int bp_event_destroy(void* ev);
+
+/* CUDA-graph capture of everything issued on `stream` (and on streams that
+ * join it through events) between begin and end; launch replays it. */
+BP_API int bp_graph_begin(void* stream);
+BP_API int bp_graph_end(void* stream, void** graph_exec_out);
+BP_API int bp_graph_launch(void* graph_exec, void* stream);
+BP_API int bp_graph_destroy(void* graph_exec);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BITPIPE_B200_COMM_H */

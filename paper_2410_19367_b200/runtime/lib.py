@@ -64,6 +64,29 @@ _SIGS = {
                        _vp]),
     "bp_adam_dev": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _f32, _f32, _f32, _f32, _i32, _vp,
                            _f32, _vp]),
+    # include/bitpipe_comm.h: runtime context (NCCL via dlopen), slots, events, graphs
+    "bp_comm_available": (_i32, []),
+    "bp_nccl_unique_id": (_i32, [_vp]),
+    "bp_init": (_i32, [_i32, _i32, _vp, _i32, ctypes.POINTER(_vp)]),
+    "bp_comm_split": (_i32, [_vp, _i32, _i32, ctypes.POINTER(_vp)]),
+    "bp_comm_rank": (_i32, [_vp]),
+    "bp_comm_size": (_i32, [_vp]),
+    "bp_slots_alloc": (_i32, [_vp, ctypes.c_size_t, _i32, ctypes.POINTER(_vp)]),
+    "bp_slot_stride": (ctypes.c_size_t, [ctypes.c_size_t]),
+    "bp_send": (_i32, [_vp, _i32, _vp, ctypes.c_size_t, _vp]),
+    "bp_recv": (_i32, [_vp, _i32, _vp, ctypes.c_size_t, _vp]),
+    "bp_group_start": (_i32, []),
+    "bp_group_end": (_i32, []),
+    "bp_allreduce_mean": (_i32, [_vp, _vp, ctypes.c_size_t, _i32, _vp]),
+    "bp_destroy": (_i32, [_vp]),
+    "bp_event_create": (_i32, [ctypes.POINTER(_vp)]),
+    "bp_event_record": (_i32, [_vp, _vp]),
+    "bp_stream_wait_event": (_i32, [_vp, _vp]),
+    "bp_event_destroy": (_i32, [_vp]),
+    "bp_graph_begin": (_i32, [_vp]),
+    "bp_graph_end": (_i32, [_vp, ctypes.POINTER(_vp)]),
+    "bp_graph_launch": (_i32, [_vp, _vp]),
+    "bp_graph_destroy": (_i32, [_vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -1,5 +1,6 @@
 """The C-ABI library loads on a CPU-only host and exports exactly what
-include/bitpipe.h declares (no compute calls without a GPU)."""
+include/bitpipe.h and include/bitpipe_comm.h declare (no compute calls
+without a GPU)."""
 import ctypes
 import os
 import re
@@ -7,11 +8,11 @@ import re
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADER = os.path.join(ROOT, "include", "bitpipe.h")
+HEADERS = [os.path.join(ROOT, "include", h) for h in ("bitpipe.h", "bitpipe_comm.h")]
 
 
 def declared():
-    text = open(HEADER).read()
+    text = "".join(open(h).read() for h in HEADERS)
     return sorted(set(re.findall(r"BP_API\s+[\w\s\*]+?\b(bp_\w+)\s*\(", text)))
 
 
@@ -44,3 +45,23 @@ def test_error_path_without_gpu():
     g.M, g.N, g.K = 0, 16, 16
     rc = h.bp_gemm(ctypes.byref(g), None)
     assert rc == 1 and b"bad shape" in h.bp_last_error()
+
+
+def test_comm_context_without_gpu():
+    """The runtime context resolves NCCL at run time (no link dependency);
+    argument errors come back as codes + messages; a unique id needs no GPU."""
+    import ctypes as C
+    from paper_2410_19367_b200.runtime import lib as L
+    if not os.path.exists(L.LIB_PATH):
+        pytest.skip("library not built")
+    h = L.lib()
+    assert "bp_allreduce_mean" in declared() and "bp_graph_launch" in declared()
+    assert h.bp_slot_stride(1) == 256 and h.bp_slot_stride(256) == 256 and h.bp_slot_stride(8 << 20) == 8 << 20
+    out = C.c_void_p()
+    assert h.bp_slots_alloc(None, 16, 1, C.byref(out)) == 1 and b"invalid" in h.bp_last_error()
+    if not h.bp_comm_available():
+        pytest.skip("no NCCL library on this host")
+    assert h.bp_init(0, 1, None, 0, C.byref(out)) == 1
+    uid = (C.c_ubyte * 128)()
+    assert h.bp_nccl_unique_id(uid) == 0
+    assert any(uid)
