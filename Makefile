@@ -22,7 +22,15 @@ build/%.cpp.o: $(PKG)/csrc/%.cpp include/bitpipe.h include/bitpipe_comm.h
 $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -cudart static -ldl
 
-clean:
-	rm -rf build $(LIB)
+# phase-traced build for tools/attn_trace.py and tools/gemm_trace.py (not the product)
+TRACE_LIB := tools/libbitpipe_trace.so
+trace: $(TRACE_LIB)
+$(TRACE_LIB): $(SRC) $(PKG)/csrc/*.cuh include/bitpipe.h include/bitpipe_comm.h
+	@mkdir -p build_trace
+	for f in $(SRC); do $(NVCC) $(NVFLAGS) -DBP_ATTN_TRACE -DBP_GEMM_TRACE -c $$f -o build_trace/$$(basename $$f).o || exit 1; done
+	$(NVCC) $(ARCH) -shared -o $@ build_trace/*.o -cudart static -ldl
 
-.PHONY: all clean
+clean:
+	rm -rf build build_trace $(LIB)
+
+.PHONY: all clean trace

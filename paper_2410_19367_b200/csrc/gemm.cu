@@ -279,6 +279,24 @@ BP_DEV void unstage_row32_bf16(const uint8_t* unit, int lane, float (&x)[32]) {
   }
 }
 
+// Phase timestamps of every CTA of the last traced 2-SM GEMM launch
+// (BP_GEMM_TRACE builds only, tools/gemm_trace.py): clock64 at entry, after
+// the prologue, first operand stage landed, last MMA issued, accumulator
+// ready in the epilogue, epilogue issued, stores drained, exit; then the
+// global timer at entry and the CTA's tile count.
+#ifdef BP_GEMM_TRACE
+__device__ long long g_gemm_trace[2 * 160][10];
+__device__ long long g_gemm_etrace[2 * 160][8][5];  // first tile, epilogue warp 0: per-chunk stamps
+#define GTRACE(k) (g_gemm_trace[blockIdx.x][k] = clock64())
+#define ETRACE(c, k) \
+  do {                                                                                         \
+    if (etr && lane == 0 && (c) < 8) g_gemm_etrace[blockIdx.x][c][k] = clock64();            \
+  } while (0)
+#else
+#define GTRACE(k) ((void)0)
+#define ETRACE(c, k) ((void)0)
+#endif
+
 // Per-warp state of the TMA epilogue, carried across tiles.
 struct EpiTma {
   uint8_t* stage;    // 2 units x 4 KB: [0, 2K) output / [2K, 4K) aux-out or input
@@ -299,7 +317,7 @@ BP_DEV void epi_tma_prefetch_input(const CUtensorMap* mx, EpiTma& es, int u, int
 
 template <int NCHUNK>
 BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap* mx, uint32_t tmem_addr,
-                         int row0, int lane, int n0, EpiTma& es, bool input_issued) {
+                         int row0, int lane, int n0, EpiTma& es, bool input_issued, bool etr = false) {
   const bool gelu = ep.epilogue == BP_EPI_GELU;
   const bool has_in = ep.residual != nullptr || ep.epilogue == BP_EPI_DGELU;
   if (has_in && !input_issued && lane == 0) epi_tma_prefetch_input(mx, es, es.ubuf, n0, row0);
@@ -311,8 +329,10 @@ BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap
     uint8_t* unit = es.stage + u * 4096;
     if (has_in && lane == 0 && c + 1 < NCHUNK && c0 + 32 < ep.N)
       epi_tma_prefetch_input(mx, es, u ^ 1, c0 + 32, row0);
+    ETRACE(c, 0);
     float v[32];
     tmem_ld_32x32b_x32(tmem_addr + c * 32, v);
+    ETRACE(c, 1);
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] *= ep.alpha;
     if (ep.bias) {
@@ -324,6 +344,7 @@ BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap
     if (has_in) {
       float cur[32];
       mbar_wait(&es.bar[u], (es.phase >> u) & 1);
+      ETRACE(c, 2);
       es.phase ^= 1u << u;
       unstage_row32_bf16(unit + 2048, lane, cur);
       if (ep.epilogue == BP_EPI_DGELU) {
@@ -336,6 +357,7 @@ BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap
     }
     if (lane == 0) bulk_wait_read<1>();  // this unit's previous store has read it
     __syncwarp();
+    ETRACE(c, 3);
     if (gelu) {
       stage_row32(unit + 2048, lane, ep.c_dtype, v);  // pre-activation -> aux
       if (ep.c_dtype == BP_BF16) {
@@ -364,6 +386,7 @@ BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap
       if (gelu) tma_store_2d(mx, unit + 2048, c0, row0);
       bulk_commit();
     }
+    ETRACE(c, 4);
     es.ubuf ^= 1;
   }
 }
@@ -642,6 +665,15 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   SkSched sch;
   sch.init(num_tiles, kblocks, ncl, cid, ws.enable);
   const int nseg = sch.count();
+#ifdef BP_GEMM_TRACE
+  if (threadIdx.x == 0) {
+    GTRACE(0);
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    g_gemm_trace[blockIdx.x][8] = (long long)gt;
+    g_gemm_trace[blockIdx.x][9] = nseg;
+  }
+#endif
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
@@ -664,6 +696,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) GTRACE(1);
 
   if (warp == 0) {
     if (lane == 0) {  // -------------------------- TMA producer (both CTAs)
@@ -720,6 +753,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         const uint32_t d_tmem = tmem_base + acc * C::BN;
         for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
+          if (si == 0 && kb == sg.kb0) GTRACE(2);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
@@ -740,6 +774,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         }
         tc_commit_2sm_mc(&tfull[acc]);
       }
+      GTRACE(3);
     }
   } else if (warp >= 4) {  // ---------------------- epilogue (both CTAs)
     const int ew = warp - 4;
@@ -760,6 +795,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       // the first input tile is requested before waiting for the accumulator
       if (tma_in && sg.role == 0 && lane == 0) epi_tma_prefetch_input(&map_aux, es, es.ubuf, n0, m0 + ew * 32);
       mbar_wait(&tfull[acc], acc_phase);
+      if (si == 0 && ew == 0 && lane == 0) GTRACE(4);
       tc_fence_after();
       const int row = m0 + ew * 32 + lane;
       const int lrow = ew * 32 + lane;  // row within this CTA's half tile
@@ -812,7 +848,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           if (n0 + c * 32 < N) epi_row32(ep, row, n0 + c * 32, v);
         }
       } else if (ep.tma_store) {
-        epi_tile_tma<C::BN / 32>(ep, &map_c, &map_aux, t0, m0 + ew * 32, lane, n0, es, tma_in);
+        epi_tile_tma<C::BN / 32>(ep, &map_c, &map_aux, t0, m0 + ew * 32, lane, n0, es, tma_in, si == 0 && ew == 0);
       } else {
         epi_tile<C::BN / 32>(ep, t0, row, n0);
       }
@@ -822,11 +858,14 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       else
         mbar_arrive_remote(&tempty[acc], 0);
     }
+    if (ew == 0 && lane == 0) GTRACE(5);
     if (ep.tma_store && lane == 0) bulk_wait<0>();  // stores complete before the CTA retires
+    if (ew == 0 && lane == 0) GTRACE(6);
   }
   __syncthreads();
   cluster_sync();
   if (warp == 2) tmem_dealloc_2sm<C::TMEM_COLS>(tmem_base);
+  if (threadIdx.x == 0) GTRACE(7);
 }
 
 // ======================================================== SIMT kernel ====
@@ -1207,4 +1246,20 @@ extern "C" int bp_gemm(const bp_gemm_args* gp, void* stream) {
   count_launch();
   BP_CHECK_LAUNCH("gemm_simt");
   return gemm_colsum_after(g, st);
+}
+
+// Debug aid (BP_GEMM_TRACE builds): copy the per-CTA phase stamps of the
+// last 2-SM GEMM launch ([2 * 160][10] long long).
+extern "C" __attribute__((visibility("default"))) int bp_gemm_trace_dump(long long* host, int n) {
+#ifdef BP_GEMM_TRACE
+  const int cap = 2 * 160 * 10, ecap = 2 * 160 * 8 * 5;
+  if (cudaMemcpyFromSymbol(host, bp::g_gemm_trace, sizeof(long long) * (n < cap ? n : cap)) != cudaSuccess) return 2;
+  if (n >= cap + ecap &&
+      cudaMemcpyFromSymbol(host + cap, bp::g_gemm_etrace, sizeof(long long) * ecap) != cudaSuccess)
+    return 2;
+  return 0;
+#else
+  (void)host; (void)n;
+  return 3;
+#endif
 }
