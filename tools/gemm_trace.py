@@ -26,6 +26,8 @@ SHAPES = [  # name, M, N, K, kwargs builder
     ("qkv fprop (bias)", 2048, 3 * h, h),
     ("fc1 fprop (gelu)", 2048, 4 * h, h),
     ("fc2 fprop (bias+res)", 2048, h, 4 * h),
+    ("fc1 dgrad (plain)", 2048, h, 4 * h),
+    ("proj fprop (plain)", 2048, h, h),
 ]
 lib = L.lib()
 dump = lib.bp_gemm_trace_dump
@@ -35,10 +37,13 @@ print(f"{'shape':24s} {'ms/launch':>9s} {'CTAs':>5s} {'tiles':>5s} {'start sprea
       + " ".join(f"{n:>10s}" for n in names) + "   (median cycles; max in brackets)")
 for name, M, N, K in SHAPES:
     a = torch.randn(M, K, device=dev).to(bf)
-    w = torch.randn(N, K, device=dev).to(bf) * 0.02
+    dgrad = "dgrad" in name
+    w = (torch.randn(K, N, device=dev) if dgrad else torch.randn(N, K, device=dev)).to(bf) * 0.02
     c = torch.empty(M, N, device=dev, dtype=bf)
     bias = torch.randn(N, device=dev).to(bf)
-    kw = {"bias": bias}
+    kw = {} if "plain" in name else {"bias": bias}
+    if dgrad:
+        kw["b_kmajor"] = False
     if "res" in name:
         kw["residual"] = torch.randn(M, N, device=dev).to(bf)
     if "gelu" in name:
