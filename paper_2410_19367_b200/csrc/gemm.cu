@@ -317,7 +317,8 @@ BP_DEV void epi_tma_prefetch_input(const CUtensorMap* mx, EpiTma& es, int u, int
 
 template <int NCHUNK>
 BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap* mx, uint32_t tmem_addr,
-                         int row0, int lane, int n0, EpiTma& es, bool input_issued, bool etr = false) {
+                         int row0, int lane, int n0, EpiTma& es, bool input_issued, bool etr = false,
+                         const float* sbias = nullptr) {
   const bool gelu = ep.epilogue == BP_EPI_GELU;
   const bool has_in = ep.residual != nullptr || ep.epilogue == BP_EPI_DGELU;
   if (has_in && !input_issued && lane == 0) epi_tma_prefetch_input(mx, es, es.ubuf, n0, row0);
@@ -335,7 +336,14 @@ BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap
     ETRACE(c, 1);
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] *= ep.alpha;
-    if (ep.bias) {
+    if (sbias) {  // the tile's bias, staged in shared memory (broadcast reads)
+      const float4* q = reinterpret_cast<const float4*>(sbias + c * 32);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 t = q[i];
+        v[4 * i] += t.x; v[4 * i + 1] += t.y; v[4 * i + 2] += t.z; v[4 * i + 3] += t.w;
+      }
+    } else if (ep.bias) {
       float t[32];
       load32(ep.bias, ep.bias_dtype, c0, t);
 #pragma unroll
@@ -628,12 +636,13 @@ struct Tc2Cfg {
   static constexpr uint32_t SUB_BYTES = B_MN_ ? BCH * 64 * BK * 2 : SUBH * BK * 2;
   static constexpr uint32_t B_BYTES = NSUB * SUB_BYTES;
   static constexpr uint32_t EPI_BYTES = 4 * 2 * 4096;  // 2 TMA-store staging units per epilogue warp
-  static constexpr int STAGE_BUDGET = 232448 - 1024 - 256 - (int)EPI_BYTES;
+  static constexpr uint32_t BIAS_BYTES = 4 * BN_;       // the tile's bias columns (fp32)
+  static constexpr int STAGE_BUDGET = 232448 - 1024 - 256 - (int)EPI_BYTES - (int)BIAS_BYTES;
   static constexpr int STAGES = STAGE_BUDGET / (A_BYTES + B_BYTES) > 8 ? 8 : STAGE_BUDGET / (A_BYTES + B_BYTES);
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int ACC = 2 * BN_ <= 512 ? 2 : 1;  // TMEM accumulator buffers
   static constexpr uint32_t TMEM_COLS = ACC * BN_ <= 256 ? 256 : 512;  // power of two
-  static constexpr size_t SMEM = 1024 + STAGES * (size_t)STAGE_BYTES + EPI_BYTES + 256;
+  static constexpr size_t SMEM = 1024 + STAGES * (size_t)STAGE_BYTES + EPI_BYTES + BIAS_BYTES + 256;
 };
 
 template <int BN, bool A_MN, bool B_MN>
@@ -648,7 +657,8 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::A_BYTES;
   uint8_t* sEpi = sB + STAGES * C::B_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + C::EPI_BYTES);
+  float* sBias = reinterpret_cast<float*>(sEpi + C::EPI_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + C::EPI_BYTES + C::BIAS_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -794,6 +804,16 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       const int n0 = (tile / tiles_m) * C::BN;
       // the first input tile is requested before waiting for the accumulator
       if (tma_in && sg.role == 0 && lane == 0) epi_tma_prefetch_input(&map_aux, es, es.ubuf, n0, m0 + ew * 32);
+      // the tile's bias columns into shared memory, also before the wait: a
+      // per-chunk bias load put an L2 round trip on every 32-column chunk
+      // (~4 k cycles of a single-tile epilogue, tools/gemm_trace.py)
+      const bool sbias = ep.tma_store && ep.bias && sg.role == 0;
+      if (sbias) {
+        epi_bar();  // every epilogue warp is done with the previous tile's bias
+        for (int j = ew * 32 + lane; j < C::BN; j += 128)
+          sBias[j] = n0 + j < N ? ld_any(ep.bias, ep.bias_dtype, n0 + j) : 0.f;
+        epi_bar();
+      }
       mbar_wait(&tfull[acc], acc_phase);
       if (si == 0 && ew == 0 && lane == 0) GTRACE(4);
       tc_fence_after();
@@ -848,7 +868,8 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           if (n0 + c * 32 < N) epi_row32(ep, row, n0 + c * 32, v);
         }
       } else if (ep.tma_store) {
-        epi_tile_tma<C::BN / 32>(ep, &map_c, &map_aux, t0, m0 + ew * 32, lane, n0, es, tma_in, si == 0 && ew == 0);
+        epi_tile_tma<C::BN / 32>(ep, &map_c, &map_aux, t0, m0 + ew * 32, lane, n0, es, tma_in, si == 0 && ew == 0,
+                                 sbias ? sBias : nullptr);
       } else {
         epi_tile<C::BN / 32>(ep, t0, row, n0);
       }

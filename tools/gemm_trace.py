@@ -28,6 +28,8 @@ SHAPES = [  # name, M, N, K, kwargs builder
     ("fc2 fprop (bias+res)", 2048, h, 4 * h),
     ("fc1 dgrad (plain)", 2048, h, 4 * h),
     ("proj fprop (plain)", 2048, h, h),
+    ("proj fprop (bias)", 2048, h, h),
+    ("proj fprop (res)", 2048, h, h),
 ]
 lib = L.lib()
 dump = lib.bp_gemm_trace_dump
@@ -41,7 +43,7 @@ for name, M, N, K in SHAPES:
     w = (torch.randn(K, N, device=dev) if dgrad else torch.randn(N, K, device=dev)).to(bf) * 0.02
     c = torch.empty(M, N, device=dev, dtype=bf)
     bias = torch.randn(N, device=dev).to(bf)
-    kw = {} if "plain" in name else {"bias": bias}
+    kw = {} if ("plain" in name or name.endswith("(res)")) else {"bias": bias}
     if dgrad:
         kw["b_kmajor"] = False
     if "res" in name:
