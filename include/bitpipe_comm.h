@@ -16,8 +16,8 @@
  *   bp_graph_*                -> CUDA-graph capture / replay of a step
  * The in-tree Python executor makes the same calls through torch.distributed
  * (NCCL) and torch.cuda.CUDAGraph; both paths use the same NCCL library
- * (loaded with dlopen("libnccl.so.2"), so a process that already loaded
- * torch's NCCL shares it).
+ * (resolved with dlopen("libnccl.so.2"), reusing the copy torch already
+ * loaded).
  *
  * Conventions as in bitpipe.h: device pointers owned by the caller, streams
  * as void*, int status (BP_OK / BP_ERR_*) with bp_last_error().  NCCL
@@ -42,7 +42,10 @@ extern "C" {
 
 typedef struct bp_ctx bp_ctx;
 
-/* 1 if an NCCL library could be loaded (no device work). */
+/* 1 if an NCCL library is already loaded in the process (no loading, no
+ * device work).  The other communicator calls load libnccl.so.2 on first use
+ * when none is; a host that also uses torch must import torch first (its
+ * libtorch_cuda needs its own NCCL build under the same soname). */
 BP_API int bp_comm_available(void);
 /* A fresh NCCL unique id (rank 0 creates it, the host broadcasts the 128
  * bytes to every rank out of band). */

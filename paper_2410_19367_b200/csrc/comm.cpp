@@ -46,8 +46,12 @@ Nccl& nccl() {
   static Nccl n;
   static std::once_flag once;
   std::call_once(once, [] {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    // Prefer the NCCL already in the process (torch's): loading another
+    // libnccl.so.2 first would satisfy torch's own dependency on that soname
+    // later and break its import.  Otherwise load one privately.
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
     if (!h) return;
 #define BP_SYM(field, name) n.field = reinterpret_cast<decltype(n.field)>(dlsym(h, name))
     BP_SYM(GetUniqueId, "ncclGetUniqueId");
@@ -93,7 +97,13 @@ cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 
 extern "C" {
 
-int bp_comm_available(void) { return nccl().ok ? 1 : 0; }
+int bp_comm_available(void) {
+  // no loading here (see nccl()): 1 when an NCCL is already in the process
+  // or was loaded by an earlier bp_* communicator call
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_NOLOAD);
+  return h && nccl().ok ? 1 : 0;
+}
 
 int bp_nccl_unique_id(void* id_out) {
   if (int rc = need_nccl()) return rc;

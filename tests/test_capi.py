@@ -51,6 +51,8 @@ def test_comm_context_without_gpu():
     """The runtime context resolves NCCL at run time (no link dependency);
     argument errors come back as codes + messages; a unique id needs no GPU."""
     import ctypes as C
+
+    import torch  # noqa: F401  -- torch's NCCL first (see bitpipe_comm.h)
     from paper_2410_19367_b200.runtime import lib as L
     if not os.path.exists(L.LIB_PATH):
         pytest.skip("library not built")
