@@ -123,8 +123,50 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def plan(args, D):
+    """(approach, layout policy, schedule) of the benchmarked configuration."""
+    from paper_2410_19367_b200 import schedule as ps
+    N = args.N
+    approach = ps.ApproachId.parse(args.approach)
+    policy = None
+    if approach is ps.ApproachId.BITPIPE and args.order != "default":
+        if (args.order == "paper" or args.paper_policy) and D in ps.PAPER_GATE_STAGE and args.max_peak is None:
+            policy = ps.paper_policy(D)
+        else:
+            policy = ps.search_bitpipe_policy(D, N, 2, max_peak=args.max_peak)[0]
+    if approach in (ps.ApproachId.BITPIPE, ps.ApproachId.BITPIPE_EARLY_FORWARD):
+        sched = ps.build_bitpipe(D, N, 2, approach is ps.ApproachId.BITPIPE_EARLY_FORWARD, policy=policy)
+    else:
+        sched = ps.build(approach, D, N)
+    return approach, policy, sched
+
+
+def workload_config(cfg, args, approach, policy, sched, G, W):
+    """The ``config`` object of the JSON line (identical for both arms)."""
+    from paper_2410_19367_b200.model import balanced_counts, stage_partition
+    D, N = sched.D, sched.N
+    counts = (balanced_counts(cfg, sched) if args.partition == "balanced"
+              else [len(p.halfblocks) for p in stage_partition(cfg, sched.num_stages)])
+    M = cfg.micro_batch * cfg.seq
+    weights_gb = 2 * cfg.n_params() / 1e9
+    act_gb = N * M * cfg.hidden * 2 * 14 * cfg.layers / 1e9 / max(1, G)
+    return {"workload": f"{cfg.name} {approach.value} v=2 D={D} N={N}"
+                        + (f" (layout policy gate {policy.gate_stage})" if policy else "")
+                        + (" all logical devices co-resident on 1 GPU" if G == 1 else " one rank per GPU"),
+            "global_batch": W * N * cfg.micro_batch, "seq_len": cfg.seq, "layers": cfg.layers,
+            "hidden": cfg.hidden, "vocab": cfg.vocab,
+            "parallelism": f"pp{D} bidirectional" + (f" x dp{W}" if W > 1 else ""),
+            "partition": {"kind": args.partition, "halfblocks_per_stage": counts},
+            "l2": f"inputs larger than L2: {weights_gb:.1f} GB bf16 weights + ~{act_gb:.1f} GB of stashed "
+                  f"activations per GPU per step vs 126 MB L2 (no flush needed)"}
+
+
 def reference_arm(args):
-    """CPU restatement of the train step (oracle), bounded sample per step."""
+    """The reference's CPU path for the benchmarked configuration: the
+    oracle's CPU restatement of the train step (the reference has no numeric
+    implementation) on a bounded sample per step, plus the
+    schedule build (the reference's own CPU code, timed through the bit-exact
+    port) -- rank 0 only."""
     import torch
     from oracle.gpt_oracle import OracleConfig, layer_sample_seconds
     from paper_2410_19367_b200.model import CONFIGS, flops_per_token
@@ -135,32 +177,55 @@ def reference_arm(args):
     cfg = CONFIGS[args.config]
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
+    D = args.D or (args.gpus // args.replicas if args.gpus > 1 else 8)
+    approach, policy, sched = plan(args, D)
+    t0 = time.perf_counter()
+    plan(args, D)
+    build_ms = (time.perf_counter() - t0) * 1e3
     oc = OracleConfig(cfg.layers, cfg.hidden, cfg.heads, cfg.seq, cfg.vocab, cfg.micro_batch, cfg.causal)
     M = cfg.micro_batch * cfg.seq
     layer_flops = 3.0 * (24 * cfg.hidden ** 2 + 4 * cfg.seq * cfg.hidden) * M
     scale = flops_per_token(cfg) * M / layer_flops  # sample -> one micro-batch through the whole model
-    for _ in range(max(1, min(args.warmup, 1))):
+    for _ in range(max(1, args.warmup)):
         layer_sample_seconds(oc)
     times = [layer_sample_seconds(oc) for _ in range(max(1, args.steps))]
     t = statistics.median(times)
     value = M / (t * scale)
-    D = args.D or 8
+    W = args.replicas
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
-        "steps": len(times), "warmup": 1, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} {args.approach} D={D} N={args.N} (CPU sample)",
-                   "global_batch": args.N * cfg.micro_batch, "seq_len": cfg.seq},
+        "steps": len(times), "warmup": max(1, args.warmup), "ms_per_step": t * scale * args.N * W * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(cfg, args, approach, policy, sched, args.gpus, W),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
-                         "sample": f"fwd+bwd of 1 transformer layer on 1 micro-batch ({M} tokens), fp32 torch CPU, "
-                                   f"extrapolated by model FLOPs (x{scale:.1f}) to whole-model tokens/s"},
+                         "sample": f"each step: fwd+bwd of 1 transformer layer on 1 micro-batch ({M} tokens), fp32 "
+                                   f"torch CPU (oracle restatement of SPEC run_schedule_numeric), extrapolated by "
+                                   f"model FLOPs (x{scale:.1f}) to whole-model tokens/s; ms_per_step = the "
+                                   f"extrapolated full step",
+                         "schedule_build_ms": build_ms},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def _self_launch(args) -> int:
+    """``--gpus N`` without a torchrun environment: launch N ranks (one
+    process per GPU) through torch.distributed.run on this node and return
+    its exit code; rank 0 prints the JSON line."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_self_launch(args))
     if args.impl == "reference":
         return reference_arm(args)
 
@@ -174,28 +239,26 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     cfg = CONFIGS[args.config]
     dist_ctx = None
+    transport = os.environ.get("BP_TRANSPORT", "peer" if args.replicas == 1 else "nccl")
     if world > 1:
-        from paper_2410_19367_b200.runtime.distributed import DistContext
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-        dist_ctx = DistContext(rank, world, replicas=args.replicas)
+        if transport == "peer":   # CUDA IPC peer memory + stream-ordered flags; gloo for the handle exchange
+            from paper_2410_19367_b200.runtime.peer import PeerContext
+            dist.init_process_group("gloo")
+            dist_ctx = PeerContext(rank, world)
+        else:                     # NCCL P2P + per-stage 2-rank all-reduce
+            from paper_2410_19367_b200.runtime.distributed import DistContext
+            dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device(f"cuda:{local}"))
+            dist_ctx = DistContext(rank, world, replicas=args.replicas)
         D = dist_ctx.D
     else:
         D = args.D or 8
     N = args.N
-    approach = ps.ApproachId.parse(args.approach)
-    policy = None
-    if approach is ps.ApproachId.BITPIPE and args.order != "default":
-        if (args.order == "paper" or args.paper_policy) and D in ps.PAPER_GATE_STAGE and args.max_peak is None:
-            policy = ps.paper_policy(D)
-        else:
-            policy = ps.search_bitpipe_policy(D, N, 2, max_peak=args.max_peak)[0]
-    if approach in (ps.ApproachId.BITPIPE, ps.ApproachId.BITPIPE_EARLY_FORWARD):
-        sched = ps.build_bitpipe(D, N, 2, approach is ps.ApproachId.BITPIPE_EARLY_FORWARD, policy=policy)
-    else:
-        sched = ps.build(approach, D, N)
+    approach, policy, sched = plan(args, D)
     tr = Trainer(cfg, sched, dtype=torch.bfloat16, optim=OptimConfig(), dist_ctx=dist_ctx, partition=args.partition)
     W = dist_ctx.replicas if dist_ctx is not None else 1
     tok, tgt = synthetic_batch(cfg, N, seed=1234 + (dist_ctx.w if dist_ctx is not None else 0))  # replica's batch
@@ -234,8 +297,8 @@ def main():
     if graphed:  # replays launch on the device without passing through the host wrappers
         launches = launches_per_step * args.steps
     ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
+    if world > 1:   # device time, max over ranks
+        t = torch.tensor([ms])
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = t.item()
     tokens_per_step = W * N * cfg.micro_batch * cfg.seq   # whole job: every pipeline replica
@@ -256,7 +319,7 @@ def main():
         barrier()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
         if world > 1:
-            t = torch.tensor([e2e_ms], device="cuda")
+            t = torch.tensor([e2e_ms])
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = t.item()
         e2e = {"value": tokens_per_step / (e2e_ms / 1e3), "unit": "tokens/s",
@@ -265,10 +328,30 @@ def main():
 
     # ---- bubble of the executed order under the measured task times
     replay = None
+    measured = None
     if world == 1:
         times = tr.measure_task_times()
         replay = tr.replay_bubble(times)
         replay["tokens_per_s_on_D_gpus"] = tokens_per_step / (replay["makespan_ms"] / 1e3)
+    else:
+        # one more step with per-task CUDA events on every rank (relative to a
+        # start event recorded right after a barrier), gathered to rank 0:
+        # beta = 1 - sum_d busy_d / (D * makespan)
+        barrier()
+        tr.record_timeline = True
+        tr.train_step(tok_d, tgt_d)
+        torch.cuda.synchronize()
+        tr.record_timeline = False
+        spans = tr.timeline_spans()
+        allspans = [None] * world
+        dist.all_gather_object(allspans, spans)
+        busy = sum(x["busy_ms"] for x in allspans)
+        t0 = min(x["start_ms"] for x in allspans)
+        t1 = max(x["end_ms"] for x in allspans)
+        measured = {"bubble": 1 - busy / (world * (t1 - t0)), "makespan_ms": t1 - t0,
+                    "busy_ms_per_rank": [x["busy_ms"] for x in allspans],
+                    "how": "per-task CUDA events on each rank's compute + weight-gradient streams, one extra step, "
+                           "times relative to a per-rank start event recorded after a barrier"}
 
     # ---- roofline: whole step and the dominant kernel (tcgen05 GEMM)
     peak_burst, peak_sust, hbm, peak_kind = _peaks()
@@ -285,9 +368,11 @@ def main():
     # launch's span is its own device time (in the concurrent step the spans
     # overlap other streams' kernels).  Serialised step time is reported too.
     Mtok = cfg.micro_batch * cfg.seq
+    # (distributed: each rank's compute and weight-gradient streams serialised
+    # likewise; its per-stage optimizer streams only run AdamW)
+    tr.streams = {d: main_stream for d in tr.streams}
+    tr.wstreams = {}  # weight-gradient GEMMs serialised too (their spans would include cross-stream waits)
     if world == 1:
-        tr.streams = {d: main_stream for d in tr.streams}
-        tr.wstreams = {}  # weight-gradient GEMMs serialised too (their spans would include cross-stream waits)
         tr.opt_stream, tr.opt_streams = main_stream, [main_stream]  # and the combined ones + AdamW
     tr.train_step(tok_d, tgt_d)
     torch.cuda.synchronize()
@@ -314,13 +399,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform token ids, seed 1234; random-init "
                                                             "weights N(0,0.02))",
-            "config": {"workload": f"{cfg.name} {approach.value} v=2 D={D} N={N}"
-                                   + (f" (layout policy gate {policy.gate_stage})" if policy else "")
-                                   + (" all logical devices co-resident on 1 GPU" if G == 1 else ""),
-                       "global_batch": W * N * cfg.micro_batch, "seq_len": cfg.seq, "layers": cfg.layers,
-                       "hidden": cfg.hidden, "vocab": cfg.vocab, "parallelism": f"pp{D} bidirectional" + (f" x dp{W}" if W > 1 else ""),
-                       "partition": {"kind": args.partition, "halfblocks_per_stage": tr.partition},
-                       "l2": "working set (2.6 GB weights, GBs of activations) >> 126 MB L2"},
+            "config": workload_config(cfg, args, approach, policy, sched, G, W),
             "loss_mean": loss_mean,
             "e2e": e2e,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_sust, "unit": "TFLOP/s",
@@ -346,10 +425,12 @@ def main():
                        "peak_activations_Ma": float(max(ps.peak_activations(sched))),
                        "canonical_of_reference_default_order": beta_default_order,
                        "measured_replay": replay,
+                       "measured": measured,
                        "note": "1 GPU: the D logical devices share the GPU, so pipeline bubbles are filled by other "
                                "streams; measured_replay = ASAP replay of the executed per-device orders with each "
                                "task's isolated measured device time (one GPU per logical device, free comm)"},
             "gpu_launches": launches,
+            "transport": (dist_ctx.transport if dist_ctx is not None else "co-resident (stream events)"),
             "clocks": clocks,
         }
         if rank == 0 and os.environ.get("BP_SKIP_CPU_BASELINE") != "1":

@@ -43,9 +43,11 @@ extern "C" {
 typedef struct bp_ctx bp_ctx;
 
 /* 1 if an NCCL library is already loaded in the process (no loading, no
- * device work).  The other communicator calls load libnccl.so.2 on first use
- * when none is; a host that also uses torch must import torch first (its
- * libtorch_cuda needs its own NCCL build under the same soname). */
+ * device work); 2 if none is loaded yet but libnccl.so.2 can be found (the
+ * probe loads and unloads it); 0 if there is none.  The other communicator
+ * calls load libnccl.so.2 on first use when none is loaded; that copy then
+ * stays in the process and a later torch import reuses it (same soname), so
+ * a host that also uses torch must import torch first. */
 BP_API int bp_comm_available(void);
 /* A fresh NCCL unique id (rank 0 creates it, the host broadcasts the 128
  * bytes to every rank out of band). */
@@ -90,6 +92,35 @@ BP_API int bp_graph_begin(void* stream);
 BP_API int bp_graph_end(void* stream, void** graph_exec_out);
 BP_API int bp_graph_launch(void* graph_exec, void* stream);
 BP_API int bp_graph_destroy(void* graph_exec);
+
+/* ------------------------------------------------------ peer memory ----
+ * The NCCL-free transport of the train step (runtime/peer.py): each rank
+ * exports its message-slot slab, its flag mailbox and its stage gradient
+ * buffers; a sender copies a message straight into the receiver's slot
+ * (copy engine; NVLink when the receiver is another GPU) and raises the
+ * slot's flag in the receiver's mailbox; the receiver's stream waits on the
+ * flag.  The replica pair of a stage reads each other's gradient through
+ * the imported pointer inside bp_adam (fused peer-read replica mean).
+ * Replaces, like bp_send / bp_recv / bp_allreduce_mean above, the SPEC's
+ * message passing and replica allreduce.
+ */
+#define BP_IPC_HANDLE_BYTES 64
+/* Export the allocation containing device pointer `ptr`: 64 handle bytes
+ * (cudaIpcMemHandle_t) and the byte offset of ptr inside it. */
+BP_API int bp_ipc_export(const void* ptr, void* handle_out, size_t* offset_out);
+/* Map a peer's exported allocation into this process (current device);
+ * *base_out + offset addresses the peer's pointer.  Opening one handle
+ * again returns the same mapping (reference counted). */
+BP_API int bp_ipc_open(const void* handle, void** base_out);
+BP_API int bp_ipc_close(void* base);
+/* Asynchronous copy on `stream` between any two device pointers (local,
+ * peer GPU or imported). */
+BP_API int bp_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
+/* Stream-ordered 32-bit flags (no kernel, no host): set writes `value` to
+ * `addr` after everything issued before it on `stream` (release); wait
+ * blocks `stream` until (int32)(*addr - value) >= 0. */
+BP_API int bp_flag_set(void* stream, void* addr, uint32_t value);
+BP_API int bp_flag_wait(void* stream, const void* addr, uint32_t value);
 
 #ifdef __cplusplus
 }

@@ -42,34 +42,55 @@ struct Nccl {
   ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
 };
 
-Nccl& nccl() {
-  static Nccl n;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    // Prefer the NCCL already in the process (torch's): loading another
-    // libnccl.so.2 first would satisfy torch's own dependency on that soname
-    // later and break its import.  Otherwise load one privately.
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
-    if (!h) return;
+// Resolve the NCCL entry points from a library handle (false if incomplete).
+bool resolve(Nccl& n, void* h) {
 #define BP_SYM(field, name) n.field = reinterpret_cast<decltype(n.field)>(dlsym(h, name))
-    BP_SYM(GetUniqueId, "ncclGetUniqueId");
-    BP_SYM(CommInitRank, "ncclCommInitRank");
-    BP_SYM(CommSplit, "ncclCommSplit");
-    BP_SYM(CommDestroy, "ncclCommDestroy");
-    BP_SYM(Send, "ncclSend");
-    BP_SYM(Recv, "ncclRecv");
-    BP_SYM(AllReduce, "ncclAllReduce");
-    BP_SYM(GroupStart, "ncclGroupStart");
-    BP_SYM(GroupEnd, "ncclGroupEnd");
-    BP_SYM(GetErrorString, "ncclGetErrorString");
-    BP_SYM(CommCount, "ncclCommCount");
-    BP_SYM(CommUserRank, "ncclCommUserRank");
+  BP_SYM(GetUniqueId, "ncclGetUniqueId");
+  BP_SYM(CommInitRank, "ncclCommInitRank");
+  BP_SYM(CommSplit, "ncclCommSplit");
+  BP_SYM(CommDestroy, "ncclCommDestroy");
+  BP_SYM(Send, "ncclSend");
+  BP_SYM(Recv, "ncclRecv");
+  BP_SYM(AllReduce, "ncclAllReduce");
+  BP_SYM(GroupStart, "ncclGroupStart");
+  BP_SYM(GroupEnd, "ncclGroupEnd");
+  BP_SYM(GetErrorString, "ncclGetErrorString");
+  BP_SYM(CommCount, "ncclCommCount");
+  BP_SYM(CommUserRank, "ncclCommUserRank");
 #undef BP_SYM
-    n.ok = n.GetUniqueId && n.CommInitRank && n.CommSplit && n.CommDestroy && n.Send && n.Recv && n.AllReduce &&
-           n.GroupStart && n.GroupEnd && n.GetErrorString;
-  });
+  return n.GetUniqueId && n.CommInitRank && n.CommSplit && n.CommDestroy && n.Send && n.Recv && n.AllReduce &&
+         n.GroupStart && n.GroupEnd && n.GetErrorString && n.CommCount && n.CommUserRank;
+}
+
+void* loaded_nccl() {
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_NOLOAD);
+  return h;
+}
+
+// The process's NCCL.  Prefer the copy already loaded (torch's).  With
+// `allow_load`, load libnccl.so.2 when none is: that copy stays in the
+// process, and a later torch import resolves its own libnccl.so.2 dependency
+// to it by soname (RTLD_LOCAL only limits symbol scope), so a host mixing
+// torch and this ABI must import torch first.  A failed lookup is never
+// cached: the next call retries (e.g. after torch has loaded NCCL).
+Nccl& nccl(bool allow_load = true) {
+  static Nccl n;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (n.ok) return n;
+  void* h = loaded_nccl();
+  if (!h && allow_load) {
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
+  }
+  if (h) {
+    Nccl t;
+    if (resolve(t, h)) {
+      t.ok = true;
+      n = t;
+    }
+  }
   return n;
 }
 
@@ -98,11 +119,15 @@ cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 extern "C" {
 
 int bp_comm_available(void) {
-  // no loading here (see nccl()): 1 when an NCCL is already in the process
-  // or was loaded by an earlier bp_* communicator call
-  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_NOLOAD);
-  return h && nccl().ok ? 1 : 0;
+  if (loaded_nccl()) return nccl(false).ok ? 1 : 0;
+  // not in the process yet: probe whether one can be loaded, without keeping it
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
+  if (!h) return 0;
+  Nccl t;
+  const bool ok = resolve(t, h);
+  dlclose(h);
+  return ok ? 2 : 0;
 }
 
 int bp_nccl_unique_id(void* id_out) {
@@ -158,9 +183,11 @@ int bp_comm_split(bp_ctx* ctx, int color, int key, bp_ctx** ctx_out) {
   c->device = ctx->device;
   // rank / size inside the sub-communicator (ranks of one color ordered by key)
   int n = -1, r = -1;
-  if (nccl().CommCount && nccl().CommUserRank) {
-    nccl().CommCount(sub, &n);
-    nccl().CommUserRank(sub, &r);
+  if (nccl().CommCount(sub, &n) != ncclSuccess || nccl().CommUserRank(sub, &r) != ncclSuccess || n < 1 || r < 0) {
+    bp::set_error("bp_comm_split: cannot determine rank / size of the sub-communicator");
+    nccl().CommDestroy(sub);
+    delete c;
+    return BP_ERR_COMM;
   }
   c->world = n;
   c->rank = r;

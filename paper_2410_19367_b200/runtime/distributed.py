@@ -13,13 +13,18 @@ P2P (activations forward, gradients backward)
 
 Eager gradient synchronisation
   Model stage s lives on dev_down(s) (down replica) and dev_up(s) = D-1-
-  dev_down(s) (up replica).  Each (stage) has its own 2-rank group, so the
-  two ranks may reach their last backward of s in different orders without
-  any collective-ordering constraint.  Right after a rank issues its last
-  backward of s, it issues all_reduce(SUM) of that stage's flat fp32
-  gradient on the optimizer stream followed by the fused AdamW with
-  grad_scale 1/2 (replica mean).  A 2-term fp32 sum is commutative, so both
-  replicas compute bit-identical updates.
+  dev_down(s) (up replica).  Each (stage) has its own 2-rank group AND its
+  own optimizer stream: the two ranks reach their last backwards of their
+  shared stages in different orders (BitPipe D=4 N=8 default order: rank 0
+  finishes stages [7, 0, 4, 3], rank 3 [4, 3, 7, 0]), and NCCL collectives
+  issued on ONE stream would chain (each group's NCCL stream waits for the
+  shared stream, which waits for the previous group's collective) into a
+  cross-rank cycle.  Right after a rank issues its last backward of s, it
+  issues all_reduce(SUM) of that stage's flat fp32 gradient on the stage's
+  stream followed by the fused AdamW with grad_scale 1/2 (replica mean).  A
+  2-term fp32 sum is commutative, so both replicas compute bit-identical
+  updates.  ``sync_order_acyclic`` checks the property that
+  makes this deadlock-free for a given schedule.
 
 Data parallelism over W replicated pipelines (``replicated_pipelines``,
 core.py:68; "stage replicas co-located"): world = W x D, rank
@@ -40,7 +45,7 @@ import torch.distributed as dist
 
 from ..schedule import Schedule, TaskKind
 
-__all__ = ["DistContext", "link_messages"]
+__all__ = ["DistContext", "link_messages", "stage_sync_orders", "sync_order_acyclic"]
 
 
 def link_messages(sched: Schedule) -> dict:
@@ -64,7 +69,49 @@ def link_messages(sched: Schedule) -> dict:
     return out
 
 
+def stage_sync_orders(sched: Schedule) -> dict:
+    """{device: [stage, ...]} -- the order in which each logical device
+    reaches the eager-sync point (last backward) of its stages."""
+    out = {}
+    for d, pos in sched.last_backward_positions().items():
+        out[d] = [s for (_dr, s), _i in sorted(pos.items(), key=lambda kv: kv[1])]
+    return out
+
+
+def sync_order_acyclic(sched: Schedule, *, shared_stream: bool) -> bool:
+    """Can the replica-pair collectives of ``sched`` complete?
+
+    Model: on each device, stage s's collective is issued at its last
+    backward.  With ``shared_stream`` (one optimizer stream per rank, NCCL's
+    stream semantics) a rank's collectives complete in its issue order, so
+    collective s of rank a depends on every collective a issued before it;
+    a collective completes only when both members issue it.  The resulting
+    wait-for graph over stages must be acyclic.  With one stream per stage
+    (what the executor does) there are no such edges and this is trivially
+    True."""
+    if not shared_stream:
+        return True
+    orders = stage_sync_orders(sched)
+    succ: dict = {}
+    for seq in orders.values():
+        for a, b in zip(seq, seq[1:]):
+            succ.setdefault(a, set()).add(b)
+    state: dict = {}
+
+    def cyclic(u) -> bool:
+        state[u] = 1
+        for w in succ.get(u, ()):
+            if state.get(w) == 1 or (state.get(w) is None and cyclic(w)):
+                return True
+        state[u] = 2
+        return False
+
+    return not any(state.get(u) is None and cyclic(u) for u in list(succ))
+
+
 class DistContext:
+    transport = "nccl"
+
     def __init__(self, rank: int, world: int, *, cuda: bool = True, replicas: int = 1):
         if replicas < 1 or world % replicas:
             raise ValueError(f"world {world} is not a multiple of the pipeline replica count {replicas}")
@@ -207,11 +254,14 @@ class DistContext:
         return self.recv(key, stream=trainer.streams[d])
 
     def sync_stage(self, trainer, dr, s, ev) -> None:
-        st = trainer.opt_stream
+        st = trainer.stage_stream(s)   # one stream per stage group: no cross-group chaining
         st.wait_event(ev)
         sp = trainer.stage_params[(dr, s)]
         copies = self.allreduce_stage(s, sp.grad, stream=st)
         trainer._adam((dr, s), [sp.grad], [sp.flat], st, grad_scale=1.0 / copies)
+
+    def after_join(self, trainer, main) -> None:
+        """Called once every stream of the iteration has joined ``main``."""
 
     def end_iteration(self, trainer) -> None:
         if self.slots:

@@ -211,6 +211,16 @@ class Trainer:
         import os
         nopt = max(1, int(os.environ.get("BP_OPT_STREAMS", "1")))
         self.opt_streams = [self.opt_stream] + [torch.cuda.Stream(device=self.device) for _ in range(nopt - 1)]
+        # distributed: one optimizer stream per local stage -- each stage's
+        # replica-pair sync (NCCL all-reduce or peer-read AdamW) must not be
+        # ordered behind another stage's, whose partner may reach it later
+        # (distributed.sync_order_acyclic)
+        self.stage_streams: dict = {}
+        if dist_ctx is not None:
+            for (_dr, s) in self.stage_params:
+                if s not in self.stage_streams:
+                    self.stage_streams[s] = torch.cuda.Stream(device=self.device)
+                    self.opt_streams.append(self.stage_streams[s])
         # weight-gradient GEMMs on a side stream per logical device, off the
         # critical path of the backward chain (the message to the previous
         # stage no longer waits for them; +0.5 % co-resident, more concurrency
@@ -275,6 +285,10 @@ class Trainer:
         ranked = sorted(self.local_devices, key=lambda d: (-end[d], d))
         levels = sorted(set(end[d] for d in ranked), reverse=True)
         return {d: -max(0, 2 - levels.index(end[d])) for d in ranked}  # 3 levels: -2, -1, 0
+
+    def stage_stream(self, s: int):
+        """The optimizer stream of stage ``s`` (distributed mode)."""
+        return self.stage_streams.get(s, self.opt_stream)
 
     def _dev_of(self, dr: Direction, s: int) -> int:
         return self.sched.stage_map(dr).device_of(s)
@@ -347,7 +361,8 @@ class Trainer:
 
     def _step_body(self, tokens, targets) -> StepOutput:
         main = torch.cuda.current_stream(self.device)
-        start_ev = torch.cuda.Event()
+        start_ev = torch.cuda.Event(enable_timing=self.record_timeline)
+        self._tl_start = start_ev if self.record_timeline else None
         if self.iter_done is not None:
             main.wait_event(self.iter_done)
         self.losses.zero_()
@@ -357,9 +372,9 @@ class Trainer:
             st.wait_event(start_ev)
         for st in self.opt_streams:
             st.wait_event(start_ev)
+        if self.dist is not None:   # before the gradients are zeroed: the peer transport waits there
+            self.dist.begin_iteration(self)   # until the partner has read last iteration's gradients
         self._zero_grads()
-        if self.dist is not None:
-            self.dist.begin_iteration(self)
 
         done_dirs: dict = {}
         tl = [] if self.record_timeline else None
@@ -415,6 +430,8 @@ class Trainer:
             ev.record(st)
             main.wait_event(ev)
         main.wait_event(done)
+        if self.dist is not None:
+            self.dist.after_join(self, main)
         self.iter_done = torch.cuda.Event()
         self.iter_done.record(main)
         self.timeline = tl
@@ -561,6 +578,27 @@ class Trainer:
         beta = 1 - Fraction(sum(busy)) / (self.D * mk)
         return {"makespan_ms": float(mk) / 1000, "bubble": float(beta),
                 "busy_ms_per_device": [float(b) / 1000 for b in busy]}
+
+    def timeline_spans(self) -> dict:
+        """This process's busy time and first-start / last-end (ms, relative
+        to the last step's start event) from its per-task CUDA events
+        (``record_timeline``); distributed ranks gather these for the
+        measured bubble.  Synchronises."""
+        torch.cuda.synchronize(self.device)
+        if not self.timeline or self._tl_start is None:
+            return {"busy_ms": 0.0, "start_ms": 0.0, "end_ms": 0.0, "tasks": 0}
+        z = self._tl_start
+        iv = sorted((z.elapsed_time(e0), z.elapsed_time(e1)) for _d, _t, e0, e1 in self.timeline)
+        busy, cur = 0.0, None   # union of the task intervals (a task's span may overlap the next one's)
+        for a, b in iv:
+            if cur is None or a > cur[1]:
+                if cur is not None:
+                    busy += cur[1] - cur[0]
+                cur = [a, b]
+            else:
+                cur[1] = max(cur[1], b)
+        busy += cur[1] - cur[0]
+        return {"busy_ms": busy, "start_ms": iv[0][0], "end_ms": max(b for _a, b in iv), "tasks": len(iv)}
 
     def measured_bubble(self):
         """Per-device busy time / makespan from the last step's per-task CUDA

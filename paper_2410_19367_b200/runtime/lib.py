@@ -87,6 +87,13 @@ _SIGS = {
     "bp_graph_end": (_i32, [_vp, ctypes.POINTER(_vp)]),
     "bp_graph_launch": (_i32, [_vp, _vp]),
     "bp_graph_destroy": (_i32, [_vp]),
+    # include/bitpipe_comm.h, peer memory: CUDA IPC, peer copies, stream-ordered flags
+    "bp_ipc_export": (_i32, [_vp, _vp, ctypes.POINTER(ctypes.c_size_t)]),
+    "bp_ipc_open": (_i32, [_vp, ctypes.POINTER(_vp)]),
+    "bp_ipc_close": (_i32, [_vp]),
+    "bp_memcpy_async": (_i32, [_vp, _vp, ctypes.c_size_t, _vp]),
+    "bp_flag_set": (_i32, [_vp, _vp, ctypes.c_uint32]),
+    "bp_flag_wait": (_i32, [_vp, _vp, ctypes.c_uint32]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -27,7 +27,10 @@ def _dt(t: torch.Tensor) -> int:
 
 
 def _p(t):
-    return None if t is None else ctypes.c_void_p(t.data_ptr())
+    """Device pointer of a tensor, or a raw address (an imported peer buffer)."""
+    if t is None:
+        return None
+    return ctypes.c_void_p(t if isinstance(t, int) else t.data_ptr())
 
 
 def _s(stream) -> ctypes.c_void_p:

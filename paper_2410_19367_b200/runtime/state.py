@@ -98,6 +98,7 @@ class BufferPool:
         self.device = torch.device(device)
         self.free = defaultdict(list)
         self.allocated_bytes = 0
+        self.foreign: set = set()   # data_ptr()s of buffers the pool must never take (transport slots)
 
     def get(self, shape, dtype, stream):
         """A free buffer of this shape, preferring one released on ``stream``
@@ -124,7 +125,7 @@ class BufferPool:
         """Release ``tensors`` once ``event`` (recorded on ``stream``) fires."""
         sid = stream.cuda_stream if stream is not None else None
         for t in tensors:
-            if t is not None:
+            if t is not None and t.data_ptr() not in self.foreign:
                 self.free[(tuple(t.shape), t.dtype)].append((t, event, sid))
 
     def forget_events(self) -> None:

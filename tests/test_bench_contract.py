@@ -26,3 +26,18 @@ def test_reference_arm_nonzero_rank_is_silent():
                           "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=300, cwd=ROOT,
                          env=env)
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_gpus_flag_self_launches_ranks():
+    """``--gpus 2`` without a torchrun environment launches 2 ranks itself
+    (the reference arm runs on CPU, so this needs no GPU): exactly one JSON
+    line, from rank 0, on the configuration of a 2-GPU run (D = 2)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "small",
+                          "--gpus", "2", "--steps", "1", "--warmup", "1"], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and "D=2" in line["config"]["workload"]
