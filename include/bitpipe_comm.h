@@ -121,6 +121,11 @@ BP_API int bp_memcpy_async(void* dst, const void* src, size_t bytes, void* strea
  * blocks `stream` until (int32)(*addr - value) >= 0. */
 BP_API int bp_flag_set(void* stream, void* addr, uint32_t value);
 BP_API int bp_flag_wait(void* stream, const void* addr, uint32_t value);
+/* Same wait as a one-thread polling kernel on `stream` (acquire loads,
+ * nanosleep back-off): for ranks sharing one GPU, where a stream blocked in
+ * a stream-memory wait can starve the time-sliced context that would raise
+ * the flag. */
+BP_API int bp_flag_wait_spin(void* stream, const void* addr, uint32_t value);
 
 #ifdef __cplusplus
 }

@@ -46,7 +46,7 @@ from dataclasses import dataclass
 import torch
 
 __all__ = ["OracleConfig", "StepResult", "stage_halfblocks", "sequential_baseline", "run_schedule_numeric",
-           "adamw_update"]
+           "execute_orders", "replica_mean_grads", "adamw_update"]
 
 
 @dataclass(frozen=True)
@@ -187,30 +187,32 @@ def sequential_baseline(cfg: OracleConfig, params: dict, tokens, targets, *, dty
     return StepResult(losses, grads, newp, m1, v1)
 
 
-def run_schedule_numeric(cfg: OracleConfig, schedule_json: str | dict, params: dict, tokens, targets, *,
-                         dtype=torch.float64, adam_state=None, step: int = 1, halfblocks=None) -> StepResult:
-    """Execute the reference per-device orders with message passing.
+def execute_orders(sch: dict, replicas: dict, stage_fn, N: int):
+    """Message-passing execution of the reference per-device orders (the
+    generic core of SPEC ``run_schedule_numeric``), shared
+    by the GPT oracle and the SPEC ToyModel (``oracle/toy_model.py``).
+
+    ``replicas``: {direction: {name: leaf tensor requiring grad}}, one per
+    stage-map direction.  ``stage_fn(P, stage, x_in, mb)`` runs one stage
+    forward of micro-batch ``mb`` (1-based) on replica ``P`` and returns the
+    activation (or, on the last stage, the scalar loss).  Each replica
+    averages its own N/len(dirs) micro-batches; gradients accumulate in the
+    replicas' ``.grad``.  Returns the per-micro-batch losses.
 
     Workers advance in lock-step rounds: a device runs its next task when
-    that task's input message (or micro-batch data) is present.  A message
-    for a task that is not pending, or a round where nobody can advance,
-    raises RuntimeError (SPEC ProtocolViolation / DeadlockDetected).
+    that task's input message (or micro-batch data) is present, following
+    the dataflow edges of reference ``schedules.py:181-199``.  A round in
+    which nobody can advance raises RuntimeError (SPEC DeadlockDetected),
+    as do messages left over after the flush (SPEC ProtocolViolation).
     """
-    sch = json.loads(schedule_json) if isinstance(schedule_json, str) else schedule_json
     D, v = sch["D"], sch["v"]
     S_tot = D * v
     dirs = [m["direction"] for m in sch["stage_maps"]]
-    N = tokens.shape[0]
     n_rep = N // len(dirs)  # micro-batches per replica
-    # partition: the uniform rule, or an explicit per-stage half-block list
-    # (the product's cost-balanced partition); the result is the same model
-    hbs = [list(h) for h in halfblocks] if halfblocks is not None else stage_halfblocks(cfg.layers, S_tot)
-    assert len(hbs) == S_tot and [hb for h in hbs for hb in h] == list(range(2 * cfg.layers))
-    replicas = {d: _clone_params(params, dtype) for d in dirs}
     rows = [[tuple(r[:4]) for r in dev] for dev in sch["per_device"]]
     pos = [0] * D
     acts, grads_in, stash = {}, {}, {}
-    losses = torch.zeros(N, dtype=dtype)
+    losses = [None] * N
     last = S_tot - 1
     remaining = sum(len(r) for r in rows)
     while remaining:
@@ -223,15 +225,14 @@ def run_schedule_numeric(cfg: OracleConfig, schedule_json: str | dict, params: d
                     if s > 0 and (dr, mb, s - 1) not in acts:
                         break
                     x_in = None if s == 0 else acts.pop((dr, mb, s - 1)).requires_grad_(True)
-                    out = _run_stage(P, hbs[s], x_in, cfg, first=s == 0, last=s == last,
-                                     tokens=tokens[mb - 1], targets=targets[mb - 1])
+                    out = stage_fn(P, s, x_in, mb)
                     stash[(dr, mb, s)] = (x_in, out)
                     if s == last:
                         losses[mb - 1] = out.detach()
                     else:
                         acts[(dr, mb, s)] = out.detach()
                 else:
-                    if s < last and (dr, mb, s + 1) not in grads_in:
+                    if (dr, mb, s) not in stash or (s < last and (dr, mb, s + 1) not in grads_in):
                         break
                     x_in, out = stash.pop((dr, mb, s))
                     if s == last:
@@ -247,11 +248,43 @@ def run_schedule_numeric(cfg: OracleConfig, schedule_json: str | dict, params: d
             raise RuntimeError("oracle executor deadlocked: no device can advance")
     if acts or grads_in or stash:
         raise RuntimeError("oracle executor: undelivered messages after flush")
-    names = list(params)
+    return torch.stack(losses)
+
+
+def replica_mean_grads(replicas: dict, names) -> dict:
+    """The eager replica-pair all-reduce as a mean: each
+    replica averaged its own N/2 micro-batches, so the pair mean is the
+    N-micro-batch mean."""
+    dirs = list(replicas)
     if len(dirs) == 2:
-        g = {k: (replicas[dirs[0]][k].grad + replicas[dirs[1]][k].grad) * 0.5 for k in names}
-    else:
-        g = {k: replicas[dirs[0]][k].grad.clone() for k in names}
+        return {k: (replicas[dirs[0]][k].grad + replicas[dirs[1]][k].grad) * 0.5 for k in names}
+    return {k: replicas[dirs[0]][k].grad.clone() for k in names}
+
+
+def run_schedule_numeric(cfg: OracleConfig, schedule_json: str | dict, params: dict, tokens, targets, *,
+                         dtype=torch.float64, adam_state=None, step: int = 1, halfblocks=None) -> StepResult:
+    """SPEC ``run_schedule_numeric`` for the GPT/BERT
+    model: execute the reference per-device orders (wire format of
+    ``dump_schedule``, reference ``schedules.py:301-356``) with message
+    passing (:func:`execute_orders`) on two identically initialised
+    replicas, average their gradients, then ONE AdamW update."""
+    sch = json.loads(schedule_json) if isinstance(schedule_json, str) else schedule_json
+    S_tot = sch["D"] * sch["v"]
+    dirs = [m["direction"] for m in sch["stage_maps"]]
+    # partition: the uniform rule, or an explicit per-stage half-block list
+    # (the product's cost-balanced partition); the result is the same model
+    hbs = [list(h) for h in halfblocks] if halfblocks is not None else stage_halfblocks(cfg.layers, S_tot)
+    assert len(hbs) == S_tot and [hb for h in hbs for hb in h] == list(range(2 * cfg.layers))
+    replicas = {d: _clone_params(params, dtype) for d in dirs}
+    last = S_tot - 1
+
+    def stage_fn(P, s, x_in, mb):
+        return _run_stage(P, hbs[s], x_in, cfg, first=s == 0, last=s == last,
+                          tokens=tokens[mb - 1], targets=targets[mb - 1])
+
+    losses = execute_orders(sch, replicas, stage_fn, tokens.shape[0])
+    names = list(params)
+    g = replica_mean_grads(replicas, names)
     base = {k: replicas[dirs[0]][k].detach() for k in names}
     m0, v0 = adam_state if adam_state is not None else (_zeros_like(base), _zeros_like(base))
     newp, m1, v1 = adamw_update(base, g, m0, v0, cfg, step)

@@ -109,7 +109,7 @@ class Trainer:
     def __init__(self, cfg: ModelConfig, schedule: Schedule, *, dtype=torch.bfloat16, optim: OptimConfig | None = None,
                  params: dict | None = None, seed: int = 1234, device=None, dist_ctx=None, record_timeline=False,
                  serial_streams: bool = False, partition="uniform", stream_priority=None, wgrad_stream=None,
-                 defer_wgrad=None):
+                 defer_wgrad=None, eager_sync=None):
         if not torch.cuda.is_available():
             raise RuntimeError("BitPipe Trainer needs a CUDA device (no CPU fallback)")
         ops.lib()  # fail loudly now if the kernel library is missing
@@ -138,6 +138,14 @@ class Trainer:
         self.local_devices = list(range(self.D)) if dist_ctx is None else [dist_ctx.dev]
         self.record_timeline = record_timeline
         self.step_count = 0
+        # eager gradient synchronisation: a
+        # stage's replica-pair sync + update is issued right after its last
+        # backward on the device; False = "BitPipe w/o E":
+        # every sync waits for the device's whole task list
+        if eager_sync is None:
+            import os
+            eager_sync = os.environ.get("BP_EAGER_SYNC", "1") == "1"
+        self.eager_sync = bool(eager_sync)
 
         # -- parameters: one StageParams per (direction, stage) held locally --
         if params is None:
@@ -377,6 +385,7 @@ class Trainer:
         self._zero_grads()
 
         done_dirs: dict = {}
+        deferred_syncs: list = []
         tl = [] if self.record_timeline else None
 
         def forward(d, t, x0):
@@ -417,8 +426,21 @@ class Trainer:
 
         msgs, stashes = drive(self.order, self.S, self.last_b, forward=forward, backward=backward,
                               send=self._send, recv=self._recv,
-                              stage_done=lambda dr, s, d, ev: self._stage_grads_ready(dr, s, d, ev, done_dirs),
+                              stage_done=(lambda dr, s, d, ev: self._stage_grads_ready(dr, s, d, ev, done_dirs))
+                              if self.eager_sync else (lambda *a: deferred_syncs.append(a)),
                               dev_of=self._dev_of)
+        if deferred_syncs:   # w/o eager sync: after all local computation of the device
+            dev_end = {}
+            for d in self.local_devices:
+                wst = self.wstreams.get(d)
+                if wst is not None:
+                    ev = torch.cuda.Event()
+                    ev.record(wst)
+                    self.streams[d].wait_event(ev)
+                dev_end[d] = torch.cuda.Event()
+                dev_end[d].record(self.streams[d])
+            for dr, s, d, _ev in sorted(deferred_syncs, key=lambda a: (a[2], self.last_b[a[2]][(a[0], a[1])])):
+                self._stage_grads_ready(dr, s, d, dev_end[d], done_dirs)
         if stashes or (msgs and self.dist is None):
             raise RuntimeError(f"protocol violation: {len(stashes)} stashes / {len(msgs)} messages left at flush")
         if self.dist is not None:

@@ -94,6 +94,7 @@ _SIGS = {
     "bp_memcpy_async": (_i32, [_vp, _vp, ctypes.c_size_t, _vp]),
     "bp_flag_set": (_i32, [_vp, _vp, ctypes.c_uint32]),
     "bp_flag_wait": (_i32, [_vp, _vp, ctypes.c_uint32]),
+    "bp_flag_wait_spin": (_i32, [_vp, _vp, ctypes.c_uint32]),
 }
 
 EXPORTED = tuple(_SIGS)

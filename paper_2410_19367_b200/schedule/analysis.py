@@ -8,15 +8,17 @@ bubble and to report the canonical bubble of the order actually executed.
 """
 from __future__ import annotations
 
+from dataclasses import dataclass, field
 from fractions import Fraction
 
-from .domain import ApproachId
+from .domain import ApproachId, ClusterSpec, ModelProfile, message_size
 from .errors import UnsupportedCombination
 from .layout import list_schedule
-from .plan import Schedule
+from .plan import Schedule, TaskKind
 
 __all__ = ["analytic_bubble_ratio", "analytic_makespan", "canonical_replay", "canonical_bubble",
-           "peak_activations", "search_bitpipe_policy"]
+           "peak_activations", "search_bitpipe_policy", "CommTotals", "comm_accounting",
+           "analytic_comm_count", "analytic_comm_time"]
 
 
 def analytic_bubble_ratio(approach: ApproachId, D: int, N: int, v: int = 2) -> Fraction:
@@ -115,3 +117,93 @@ def search_bitpipe_policy(D: int, N: int, v: int = 2, max_peak=None):
     if best is None:
         raise ValueError(f"no BitPipe layout policy keeps the activation peak within {max_peak} M_a")
     return best[1], best[2], best[0][0], best[3]
+
+
+# -- communication accounting (PAPER Appendix C Table 6)
+@dataclass(frozen=True)
+class CommTotals:
+    """What one iteration of a schedule moves between devices.
+
+    p2p_messages     -- cross-device stage-boundary transfers (activation on
+                        F(m,s)->F(m,s+1), gradient on B(m,s+1)->B(m,s));
+    local_copies     -- boundaries whose two stages share a device (the V
+                        map's fold; PAPER.md:101 "local copying");
+    p2p_bytes        -- p2p_messages x message_size (split intra / inter node
+                        by the cluster's devices_per_node);
+    per_link         -- {(src, dst): messages};
+    allreduce_groups -- replica-pair gradient syncs: one per (device pair
+                        (d, D-1-d), model stage both hold) for bidirectional
+                        schedules -- 2v per pair;
+    allreduce_bytes  -- per device: gradient bytes it all-reduces per
+                        iteration (grad_bytes_per_stage x stages it holds).
+    """
+    p2p_messages: int
+    local_copies: int
+    p2p_bytes: int
+    p2p_bytes_intra: int
+    p2p_bytes_inter: int
+    per_link: dict = field(default_factory=dict)
+    allreduce_groups: int = 0
+    allreduce_bytes: int = 0
+
+
+def comm_accounting(s: Schedule, profile: ModelProfile | None = None, cluster: ClusterSpec | None = None,
+                    grad_bytes_per_stage: int = 0) -> CommTotals:
+    """Count the P2P messages / bytes and allreduce volume of one iteration
+    of ``s`` from its dataflow edges (reference ``schedules.py:181-199``) and
+    stage maps.  The count for a v=2 interleaved / BitPipe pipeline is the
+    looping count minus the local-copy edges: BitPipe moves
+    N (4D - 4) messages, interleaved-looping N (4D - 2), 1F1B N (2D - 2)."""
+    msg = message_size(profile) if profile is not None else 0
+    per_node = cluster.devices_per_node if cluster is not None else max(1, s.D)
+    n_msg = n_local = intra = inter = 0
+    links: dict = {}
+    for t in s.all_tasks():
+        if t.kind is TaskKind.FORWARD and t.stage + 1 < s.num_stages:
+            nxt = t.stage + 1
+        elif t.kind is TaskKind.BACKWARD and t.stage > 0:
+            nxt = t.stage - 1
+        else:
+            continue
+        smap = s.stage_map(t.direction)
+        src, dst = smap.device_of(t.stage), smap.device_of(nxt)
+        if src == dst:
+            n_local += 1
+            continue
+        n_msg += 1
+        links[(src, dst)] = links.get((src, dst), 0) + 1
+        if src // per_node == dst // per_node:
+            intra += msg
+        else:
+            inter += msg
+    groups = 0
+    ar_bytes = 0
+    if s.is_bidirectional:
+        for d in range(s.D):
+            held = sum(len(s.stage_map(dr).stages_on(d)) for dr in s.directions)
+            groups += held if d < s.D - 1 - d else 0   # every held stage syncs with the partner
+            ar_bytes = max(ar_bytes, held * grad_bytes_per_stage)
+    return CommTotals(n_msg, n_local, n_msg * msg, intra, inter, links, groups, ar_bytes)
+
+
+def analytic_comm_count(approach: ApproachId, D: int, N: int) -> int:
+    """The message-count factor of PAPER Table 6: the
+    number of message times on the critical path of one iteration --
+    DAPPLE / Chimera 2N + 2(D-1), 1F1B-Int / BitPipe 4N + 4(D-1)."""
+    a = ApproachId(approach)
+    if a in (ApproachId.DAPPLE_1F1B, ApproachId.CHIMERA):
+        return 2 * N + 2 * (D - 1)
+    if a in (ApproachId.INTERLEAVED_LOOPING, ApproachId.BITPIPE):
+        return 4 * N + 4 * (D - 1)
+    raise UnsupportedCombination(f"Table 6 has no row for {a.value}")
+
+
+def analytic_comm_time(approach: ApproachId, D: int, N: int, profile: ModelProfile, cluster: ClusterSpec,
+                       M_grad: float = 0.0) -> float:
+    """PAPER Table 6: count x message_size / W_inter, plus
+    M_grad / W_intra for the bidirectional approaches (Chimera, BitPipe)."""
+    a = ApproachId(approach)
+    t = analytic_comm_count(a, D, N) * message_size(profile) / cluster.inter_node_bandwidth
+    if a in (ApproachId.CHIMERA, ApproachId.BITPIPE):
+        t += M_grad / cluster.intra_node_bandwidth
+    return t

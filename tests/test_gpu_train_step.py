@@ -49,7 +49,7 @@ def rel(a, b):
 
 
 def run_pair(label, text, cfg_name, dtype, tol_loss, tol_grad, check_params, partition="uniform", defer_wgrad=None,
-             expect_combined=None):
+             expect_combined=None, eager_sync=None):
     from paper_2410_19367_b200.runtime.executor import Trainer
     cfg = CONFIGS[cfg_name]
     sched = build_ours(label)
@@ -58,7 +58,7 @@ def run_pair(label, text, cfg_name, dtype, tol_loss, tol_grad, check_params, par
     params = init_params(cfg, 7, perturb=True)
     tok, tgt = synthetic_batch(cfg, sched.N, seed=11)
     tr = Trainer(cfg, sched, dtype=dtype, optim=opt, params=params, record_timeline=True, partition=partition,
-                 defer_wgrad=defer_wgrad)
+                 defer_wgrad=defer_wgrad, eager_sync=eager_sync)
     if expect_combined is not None:
         assert tr.combined_wgrad == expect_combined
     # executed per-device order == schedule order, bit for bit
@@ -184,3 +184,37 @@ def test_cuda_graph_replay_equals_eager(dtype):
     va = torch.cat([ma[k].reshape(-1) for k in sorted(ma)])
     vb = torch.cat([mb[k].reshape(-1) for k in sorted(ma)])
     assert rel(vb, va) < (1e-5 if dtype == torch.float32 else 1e-3)
+
+
+def test_spec_train_step_entry():
+    """SPEC run_schedule_numeric shape on the B200: the
+    reference wire format in, StepResult (losses, pre-update replica-mean
+    gradients, updated weights) out; a second call continues the run."""
+    from paper_2410_19367_b200.runtime.api import train_step
+    label = "D=4;N=8;approach=bitpipe;v=2"
+    text = golden()[label]
+    cfg = CONFIGS["tiny"]
+    opt = OptimConfig(lr=1e-3, weight_decay=0.01)
+    params = init_params(cfg, 7, perturb=True)
+    tok, tgt = synthetic_batch(cfg, 8, seed=11)
+    res = train_step(text, "tiny", (tok, tgt), dtype=torch.float32, optim=opt, params=params)
+    ref = run_schedule_numeric(oracle_cfg(cfg, opt), text, params, tok, tgt)
+    assert rel(res.losses, ref.losses) < 1e-4
+    assert abs(res.loss - ref.losses.mean().item()) < 1e-4 * ref.losses.mean().item()
+    assert max(rel(res.grads[k], ref.grads[k]) for k in params) < 1e-4
+    assert max(rel(res.params[k] - params[k], ref.params[k] - params[k].double()) for k in params) < 1e-3
+    tok2, tgt2 = synthetic_batch(cfg, 8, seed=12)
+    res2 = train_step(res.trainer.sched, "tiny", (tok2, tgt2), trainer=res.trainer)
+    ref2 = run_schedule_numeric(oracle_cfg(cfg, opt), text, {k: v.float() for k, v in ref.params.items()}, tok2,
+                                tgt2, adam_state=(ref.adam_m, ref.adam_v), step=2)
+    assert rel(res2.losses, ref2.losses) < 1e-4
+    with pytest.raises(ValueError, match="ShapeMismatch"):
+        train_step(text, "tiny", (tok[:4], tgt[:4]), trainer=res.trainer)
+
+
+@pytest.mark.parametrize("label", ["D=4;N=8;approach=bitpipe;v=2", "D=4;N=4;approach=chimera"])
+def test_without_eager_sync(label):
+    """"BitPipe w/o E": every replica-pair sync after the
+    device's whole task list -- same step, same numbers."""
+    tr = run_pair(label, golden()[label], "tiny", torch.float32, 1e-4, 1e-4, check_params=1e-3, eager_sync=False)
+    assert not tr.eager_sync

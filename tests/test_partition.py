@@ -75,3 +75,50 @@ def test_policy_search_generalises_f2():
 def test_peak_activations_default_order():
     """Non-EF BitPipe peaks lie in PAPER Table 2's [(D+3)/2, D] M_a (D=4 N=8 gives 3.5, 4, 4, 3.5)."""
     assert ps.peak_activations(ps.build_bitpipe(4, 8)) == [Fraction(7, 2), 4, 4, Fraction(7, 2)]
+
+
+# -- communication accounting (PAPER Appendix C Table 6; SPEC.md:280-287,354-360)
+def test_comm_accounting_counts():
+    from paper_2410_19367_b200 import schedule as ps
+    prof = lambda N: ps.ModelProfile(1, N, 2048, 2048)  # noqa: E731
+    for D in (2, 4, 8):
+        for N in (D, 2 * D, 4 * D):
+            b = ps.comm_accounting(ps.build_bitpipe(D, N), prof(N), grad_bytes_per_stage=3)
+            assert b.p2p_messages == N * (4 * D - 4)           # SURVEY §8(a) S9
+            assert b.local_copies == 2 * N                       # the V fold, F and B, every micro-batch
+            assert b.p2p_bytes == b.p2p_messages * 2 * 2048 * 2048
+            assert b.allreduce_groups == (D // 2) * 4            # 2v stages per replica pair
+            assert b.allreduce_bytes == 4 * 3
+            assert set(b.per_link) == {(d, d + 1) for d in range(D - 1)} | {(d + 1, d) for d in range(D - 1)}
+            il = ps.comm_accounting(ps.build_interleaved_looping(D, N), prof(N))
+            # looping count minus the local-copy edges (SPEC.md:282)
+            assert il.p2p_messages - b.p2p_messages == 2 * N and il.local_copies == 0
+            assert ps.comm_accounting(ps.build_1f1b(D, N), prof(N)).p2p_messages == N * 2 * (D - 1)
+    assert ps.comm_accounting(ps.build_1f1b(1, 4), prof(4)).p2p_messages == 0   # D=1: all local
+    # intra / inter split by devices_per_node: D=8 over two 4-GPU nodes, only the 3<->4 link crosses
+    c = ps.comm_accounting(ps.build_bitpipe(8, 16), prof(16), ps.ClusterSpec(8, devices_per_node=4))
+    assert c.p2p_bytes_inter == (c.per_link[(3, 4)] + c.per_link[(4, 3)]) * 2 * 2048 * 2048
+    assert c.p2p_bytes_intra + c.p2p_bytes_inter == c.p2p_bytes
+
+
+def test_analytic_comm_time_table6():
+    from fractions import Fraction
+    import pytest
+    from paper_2410_19367_b200 import schedule as ps
+    A = ps.ApproachId
+    cl = ps.ClusterSpec(4, intra_node_bandwidth=200e9, inter_node_bandwidth=25e9)
+    prof = ps.ModelProfile(1, 4, 1024, 3072)   # message_size = 6,291,456 B
+    assert ps.message_size(prof) == 6291456
+    # SPEC.md:357: DAPPLE D=4 N=4 -> 14 messages, ~3.52 ms
+    assert ps.analytic_comm_count(A.DAPPLE_1F1B, 4, 4) == 14
+    assert abs(ps.analytic_comm_time(A.DAPPLE_1F1B, 4, 4, prof, cl) - 14 * 6291456 / 25e9) < 1e-15
+    assert ps.analytic_comm_count(A.INTERLEAVED_LOOPING, 4, 4) == 28
+    # SPEC.md:358: BitPipe's P2P term is exactly 2x Chimera's; allreduce terms equal
+    for D, N in ((4, 4), (8, 16), (8, 32)):
+        mg = 1.5e9
+        b = ps.analytic_comm_time(A.BITPIPE, D, N, prof, cl, mg) - mg / 200e9
+        c = ps.analytic_comm_time(A.CHIMERA, D, N, prof, cl, mg) - mg / 200e9
+        assert abs(b - 2 * c) < 1e-12
+        assert Fraction(ps.analytic_comm_count(A.BITPIPE, D, N), ps.analytic_comm_count(A.DAPPLE_1F1B, D, N)) == 2
+    with pytest.raises(ps.errors.UnsupportedCombination):
+        ps.analytic_comm_time(A.GPIPE, 4, 4, prof, cl)
