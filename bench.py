@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="gpt-1.3b")
+    ap.add_argument("--layers", type=int, default=None,
+                    help="reduced-depth slice of --config at full width (e.g. --config gpt-10b --layers 8)")
     ap.add_argument("--approach", default="bitpipe")
     ap.add_argument("--D", type=int, default=None)
     ap.add_argument("--N", type=int, default=16)
@@ -174,7 +176,7 @@ def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = CONFIGS[args.config]
+    cfg = _model_config(args)
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
     D = args.D or (args.gpus // args.replicas if args.gpus > 1 else 8)
@@ -222,6 +224,16 @@ def _self_launch(args) -> int:
     return subprocess.run(cmd).returncode
 
 
+def _model_config(args):
+    """BASELINE config by name, optionally at reduced depth (same width)."""
+    import dataclasses
+    from paper_2410_19367_b200.model import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.layers is not None and args.layers != cfg.layers:
+        cfg = dataclasses.replace(cfg, name=f"{cfg.name}-L{args.layers}", layers=args.layers)
+    return cfg
+
+
 def main():
     args = parse()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -241,12 +253,18 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
+    # BP_SHARE_GPU=1: every rank on cuda:0 -- a functional test of the
+    # multi-rank path (transport, max-over-ranks timing, measured bubble) on a
+    # one-GPU box; its timings are NOT multi-GPU numbers (time-sliced GPU)
+    shared = os.environ.get("BP_SHARE_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
-    cfg = CONFIGS[args.config]
+    cfg = _model_config(args)
     dist_ctx = None
     transport = os.environ.get("BP_TRANSPORT", "peer" if args.replicas == 1 else "nccl")
     if world > 1:
-        if transport == "peer":   # CUDA IPC peer memory + stream-ordered flags; gloo for the handle exchange
+        if transport == "peer":   # CUDA IPC peer memory + interprocess events; gloo for the handle exchange
             from paper_2410_19367_b200.runtime.peer import PeerContext
             dist.init_process_group("gloo")
             dist_ctx = PeerContext(rank, world)
@@ -430,13 +448,20 @@ def main():
                                "streams; measured_replay = ASAP replay of the executed per-device orders with each "
                                "task's isolated measured device time (one GPU per logical device, free comm)"},
             "gpu_launches": launches,
-            "transport": (dist_ctx.transport if dist_ctx is not None else "co-resident (stream events)"),
+            "wgrad": {"deferred_stages": tr.deferred_stages, "combined_stages": sorted(tr.combined_stages),
+                      "note": "deferred = one K = N M weight-gradient GEMM per weight at the stage's last "
+                              "backward; the rest per micro-batch (slots over the memory budget)"},
+            "transport": (dist_ctx.transport if dist_ctx is not None else "co-resident (stream events)")
+                         + (" -- ALL RANKS SHARE ONE GPU (BP_SHARE_GPU=1): functional test, not a multi-GPU number"
+                            if shared else ""),
             "clocks": clocks,
         }
         if rank == 0 and os.environ.get("BP_SKIP_CPU_BASELINE") != "1":
             line["cpu_baseline"] = _cpu_baseline(cfg, args)
         print(json.dumps(line), flush=True)
     if world > 1:
+        if hasattr(dist_ctx, "close"):
+            dist_ctx.close()
         dist.destroy_process_group()
 
 

@@ -87,6 +87,11 @@ enum bp_option {
                                 (two query tiles per CTA for non-causal
                                 attention at S % 256 == 0, else one), 1 one
                                 tile per CTA, 2 two tiles                   */
+  BP_OPT_GEMM_OCC = 12,       /* 2-SM GEMM co-resident variant (two CTA pairs
+                                per SM pair, one accumulator, 2 stages):
+                                0 (default) never -- measured slower in the
+                                train step; 1 single-wave launches; 2 always
+                                (tiles <= 256 wide)                         */
 };
 BP_API int bp_set_option(int option, int value);
 

@@ -623,7 +623,14 @@ BP_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 // (M=256, N=256) reading both CTAs' smem, each CTA's TMEM receives its own
 // 128 x 256 accumulator.  Halves the per-SM operand traffic of the 1-SM
 // kernel (L2 -> SM bandwidth is the bound there).
-template <int BN_, bool B_MN_>
+// OCC = 2: the co-resident variant -- one TMEM accumulator (<= 256
+// columns) and a shared-memory budget of half an SM, so TWO CTA pairs (of
+// different kernels: the co-resident executor runs one stream per logical
+// device) share each SM pair.  A single-wave GEMM (one tile per pair: most
+// M = 2048 per-micro-batch shapes) then has its pipeline fill and epilogue
+// overlapped by the other pair's MMAs instead of leaving the tensor pipe
+// idle; no stream-K paths (its owner CTAs spin).
+template <int BN_, bool B_MN_, int OCC_ = 1>
 struct Tc2Cfg {
   // BN = pair-tile width; wider than 256 is issued as NSUB MMAs of N = 256
   // per k-step into adjacent TMEM columns (one accumulator buffer then).
@@ -637,20 +644,25 @@ struct Tc2Cfg {
   static constexpr uint32_t B_BYTES = NSUB * SUB_BYTES;
   static constexpr uint32_t EPI_BYTES = 4 * 2 * 4096;  // 2 TMA-store staging units per epilogue warp
   static constexpr uint32_t BIAS_BYTES = 4 * BN_;       // the tile's bias columns (fp32)
-  static constexpr int STAGE_BUDGET = 232448 - 1024 - 256 - (int)EPI_BYTES - (int)BIAS_BYTES;
+  static constexpr int OCC = OCC_;
+  static_assert(OCC == 1 || (OCC == 2 && BN_ <= 256), "co-resident variant: one <= 256-column accumulator");
+  // per-CTA budget: the SM's 232448 B (OCC = 1), or half of it less the
+  // 1 KB the hardware reserves per resident CTA (OCC = 2)
+  static constexpr int SM_BUDGET = OCC == 1 ? 232448 : 232448 / 2 - 1024;
+  static constexpr int STAGE_BUDGET = SM_BUDGET - 1024 - 256 - (int)EPI_BYTES - (int)BIAS_BYTES;
   static constexpr int STAGES = STAGE_BUDGET / (A_BYTES + B_BYTES) > 8 ? 8 : STAGE_BUDGET / (A_BYTES + B_BYTES);
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int ACC = 2 * BN_ <= 512 ? 2 : 1;  // TMEM accumulator buffers
+  static constexpr int ACC = (OCC == 1 && 2 * BN_ <= 512) ? 2 : 1;  // TMEM accumulator buffers
   static constexpr uint32_t TMEM_COLS = ACC * BN_ <= 256 ? 256 : 512;  // power of two
   static constexpr size_t SMEM = 1024 + STAGES * (size_t)STAGE_BYTES + EPI_BYTES + BIAS_BYTES + 256;
 };
 
-template <int BN, bool A_MN, bool B_MN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+template <int BN, bool A_MN, bool B_MN, int OCC>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, OCC)
 gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_aux,
                 int M, int N, int K, Epi ep, SkWs ws) {
-  using C = Tc2Cfg<BN, B_MN>;
+  using C = Tc2Cfg<BN, B_MN, OCC>;
   constexpr int BK = C::BK, STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -673,7 +685,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   const int kblocks = (K + BK - 1) / BK;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   SkSched sch;
-  sch.init(num_tiles, kblocks, ncl, cid, ws.enable);
+  sch.init(num_tiles, kblocks, ncl, cid, OCC == 1 ? ws.enable : 0);
   const int nseg = sch.count();
 #ifdef BP_GEMM_TRACE
   if (threadIdx.x == 0) {
@@ -820,7 +832,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       const int row = m0 + ew * 32 + lane;
       const int lrow = ew * 32 + lane;  // row within this CTA's half tile
       const uint32_t t0 = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * C::BN;
-      if (sg.role == 2) {
+      if (OCC == 1 && sg.role == 2) {
         // contributor: raw fp32 partial -> workspace slot, then publish
         float* dst = ws.part + (((size_t)cid * 2 + rank) * 128 + lrow) * C::BN;
 #pragma unroll 1
@@ -834,7 +846,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         __threadfence();
         epi_bar();
         if (ew == 0 && lane == 0) flag_release(&ws.flag[cid * 2 + rank], ws.epoch);
-      } else if (sg.role == 1) {
+      } else if (OCC == 1 && sg.role == 1) {
         // owner: wait for every contributor of this tile, add partials
         const int qlo = sch.contrib_lo(tile);
         for (int q = qlo; q < cid; ++q)
@@ -1074,9 +1086,9 @@ static int sk_workspace(cudaStream_t st, size_t floats, int nflag, SkWs* out) {
   return BP_OK;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int OCC>
 static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
-  using C = Tc2Cfg<BN, B_MN>;
+  using C = Tc2Cfg<BN, B_MN, OCC>;
   CUtensorMap ma, mb;
   int rc;
   if (!A_MN)
@@ -1103,7 +1115,7 @@ static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
       if ((rc = make_map_dt(&maux, g.residual, g.N, g.M, g.ldr, 32, 32, g.c_dtype, sw))) return rc;
     }
   }
-  auto kern = gemm_tc2_kernel<BN, A_MN, B_MN>;
+  auto kern = gemm_tc2_kernel<BN, A_MN, B_MN, OCC>;
   static bool attr_set = false;
   if (!attr_set) {
     BP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -1118,9 +1130,9 @@ static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   // MLP-down / LM-head dgrad shapes), which then use all pairs.
   const int skm = stream_k_mode();
   const int kb = (g.K + 63) / 64;
-  const bool sk_sub = skm != 2 && tiles < pairs && kb >= 64 && tiles * 2 > pairs;
+  const bool sk_sub = OCC == 1 && skm != 2 && tiles < pairs && kb >= 64 && tiles * 2 > pairs;
   if (sk_sub) npairs = pairs;
-  ws.enable = (sk_sub || (skm == 1 && tiles > npairs && tiles % npairs != 0)) ? 1 : 0;
+  ws.enable = OCC == 1 && (sk_sub || (skm == 1 && tiles > npairs && tiles % npairs != 0)) ? 1 : 0;
   if (ws.enable) {
     if (int rc = sk_workspace(st, (size_t)npairs * 2 * 128 * C::BN, npairs * 2, &ws)) return rc;
   }
@@ -1130,13 +1142,13 @@ static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   return BP_OK;
 }
 
-template <int BN>
+template <int BN, int OCC = 1>
 static int dispatch_tc2_bn(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
-  if (!amn && !bmn) return launch_tc2<BN, false, false>(g, ep, st);
-  if (!amn && bmn) return launch_tc2<BN, false, true>(g, ep, st);
-  if (amn && !bmn) return launch_tc2<BN, true, false>(g, ep, st);
-  return launch_tc2<BN, true, true>(g, ep, st);
+  if (!amn && !bmn) return launch_tc2<BN, false, false, OCC>(g, ep, st);
+  if (!amn && bmn) return launch_tc2<BN, false, true, OCC>(g, ep, st);
+  if (amn && !bmn) return launch_tc2<BN, true, false, OCC>(g, ep, st);
+  return launch_tc2<BN, true, true, OCC>(g, ep, st);
 }
 
 // Pair-tile width BN in {256, 224, 192, 128}.  Per k-block a CTA streams
@@ -1173,8 +1185,26 @@ int pick_tc2_bn(int M, int N, int pairs, bool b_mn_major) {
   return best;
 }
 
+int gemm_occ_mode();
+
 static int dispatch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
-  switch (pick_tc2_bn(g.M, g.N, num_sms() / 2, !g.b_kmajor)) {
+  const int pairs = num_sms() / 2;
+  const int bn = pick_tc2_bn(g.M, g.N, pairs, !g.b_kmajor);
+  // co-resident variant (BP_OPT_GEMM_OCC: 0 never -- the default, measured
+  // slower: GPT-1.3B step 103.4 k vs 106.7 k tok/s with it on single-wave
+  // launches, its per-launch GEMM time 92 vs 76 us: two 32 KB stages per CTA
+  // do not cover the operand latency; 1 single-wave launches; 2 always)
+  const int occm = gemm_occ_mode();
+  const long tiles = (long)((g.M + 255) / 256) * ((g.N + bn - 1) / bn);
+  if (bn <= 256 && occm != 0 && (occm == 2 || tiles <= pairs)) {
+    switch (bn) {
+      case 224: return dispatch_tc2_bn<224, 2>(g, ep, st);
+      case 192: return dispatch_tc2_bn<192, 2>(g, ep, st);
+      case 128: return dispatch_tc2_bn<128, 2>(g, ep, st);
+      default: return dispatch_tc2_bn<256, 2>(g, ep, st);
+    }
+  }
+  switch (bn) {
     case 512: return dispatch_tc2_bn<512>(g, ep, st);
     case 224: return dispatch_tc2_bn<224>(g, ep, st);
     case 192: return dispatch_tc2_bn<192>(g, ep, st);

@@ -154,13 +154,18 @@ class Trainer:
         self.stage_params: dict = {}
         self.compute: dict = {}
         grad_scale = 1.0 / self.n_rep
-        if defer_wgrad is None:  # env BP_DEFER_WGRAD=0/1 forces; default: on when the slots fit
+        if defer_wgrad is None:  # env BP_DEFER_WGRAD=0/1 forces; default: per stage, while the slots fit
             import os
             env = os.environ.get("BP_DEFER_WGRAD")
             if env is not None:
                 defer_wgrad = env == "1"
             else:
-                defer_wgrad = self._slot_bytes(dtype) <= 0.4 * torch.cuda.get_device_properties(self.device).total_memory
+                defer_wgrad = self._deferred_stages(dtype, 0.4 * torch.cuda.get_device_properties(
+                    self.device).total_memory)
+        # per-stage decision: a set of stages, or all / none
+        defer_of = (lambda s: s in defer_wgrad) if isinstance(defer_wgrad, (set, frozenset)) else \
+            (lambda s, v=bool(defer_wgrad): v)
+        self.deferred_stages = sorted(s for s in range(self.S) if defer_of(s))
         for dr in self.dirs:
             smap = schedule.stage_map(dr)
             for s in range(self.S):
@@ -175,13 +180,15 @@ class Trainer:
                     sp.load(params)
                 self.stage_params[(dr, s)] = sp
                 self.compute[(dr, s)] = StageCompute(cfg, self.plans[s], sp, grad_scale=grad_scale, n_rep=self.n_rep,
-                                                     defer_wgrad=defer_wgrad)
+                                                     defer_wgrad=defer_of(s))
         # co-resident bidirectional: one deferred weight-gradient GEMM per
         # weight over both replicas' micro-batches (shared slots, K = N M),
         # issued on the optimizer stream when both replicas are done
-        self.combined_wgrad = dist_ctx is None and self.bidir and defer_wgrad and self.n_rep > 1
+        self.combined_stages = (set(self.deferred_stages) if dist_ctx is None and self.bidir and self.n_rep > 1
+                                else set())
+        self.combined_wgrad = bool(self.combined_stages)
         if self.combined_wgrad:
-            for s in range(self.S):
+            for s in sorted(self.combined_stages):
                 c0, c1 = self.compute[(self.dirs[0], s)], self.compute[(self.dirs[1], s)]
                 c1._slots = c0._slots
                 c0.slot_total = c1.slot_total = 2 * self.n_rep
@@ -256,11 +263,12 @@ class Trainer:
         self._graph = None
 
     # ----------------------------------------------------------------- helpers --
-    def _slot_bytes(self, dtype) -> int:
+    def _slot_bytes(self, dtype, stage=None) -> int:
         """Device memory the deferred weight-gradient slots of this process's
-        stage replicas take: per half-block n_rep micro-batches of (attention)
-        a, o, dy, dqkv = 6h or (MLP) m, g, dy, du = 2h + 2 ffn columns, plus
-        LN-f output and logits on the head stage."""
+        stage replicas take (of one stage, or all): per half-block n_rep
+        micro-batches of (attention) a, o, dy, dqkv = 6h or (MLP) m, g, dy,
+        du = 2h + 2 ffn columns, plus LN-f output and logits on the head
+        stage."""
         cfg = self.cfg
         esz = torch.empty(0, dtype=dtype).element_size()
         rows = self.n_rep * cfg.micro_batch * cfg.seq
@@ -268,13 +276,35 @@ class Trainer:
         for dr in self.dirs:
             smap = self.sched.stage_map(dr)
             for s in range(self.S):
-                if smap.device_of(s) not in self.local_devices:
+                if smap.device_of(s) not in self.local_devices or (stage is not None and s != stage):
                     continue
                 for hb in self.plans[s].halfblocks:
                     total += rows * (6 * cfg.hidden if hb % 2 == 0 else 2 * cfg.hidden + 2 * cfg.ffn) * esz
                 if self.plans[s].head:
                     total += rows * (cfg.hidden + cfg.vocab) * esz
         return total
+
+    def _deferred_stages(self, dtype, budget: float) -> set:
+        """Stages whose weight gradients are deferred to one K = N M GEMM per
+        weight: all of them when their slots fit ``budget`` bytes, else the
+        stages with the most weight-GEMM work per slot byte first (the
+        per-micro-batch form stays for the rest) -- so a model too large for
+        all slots (e.g. the GPT-10B width) still defers most of its GEMMs."""
+        sizes = {s: self._slot_bytes(dtype, s) for s in range(self.S)}
+        if sum(sizes.values()) <= budget:
+            return set(range(self.S))
+        cfg = self.cfg
+
+        def work(s):   # weight-gradient FLOPs per micro-batch token of stage s
+            w = sum(8 * cfg.hidden ** 2 if hb % 2 == 0 else 2 * cfg.hidden * cfg.ffn for hb in self.plans[s].halfblocks)
+            return w + (cfg.hidden * cfg.vocab if self.plans[s].head else 0)
+
+        chosen, used = set(), 0
+        for s in sorted(range(self.S), key=lambda s: (-work(s) / max(1, sizes[s]), s)):
+            if sizes[s] and used + sizes[s] <= budget:
+                chosen.add(s)
+                used += sizes[s]
+        return chosen
 
     def _stream_priorities(self, mode) -> dict:
         """Co-resident CUDA stream priorities (lower = more urgent).  'tail':
@@ -492,7 +522,7 @@ class Trainer:
             st.wait_event(e)
         grads = [self.stage_params[(x, s)].grad for x in self.dirs]
         outs = list({id(t): t for t in (self.stage_params[(x, s)].flat for x in self.dirs)}.values())  # shared: one
-        if not self.combined_wgrad:
+        if s not in self.combined_stages:
             self._adam(s, grads, outs, st)
             return
         # both replicas' GEMM-weight gradients in one set of GEMMs into the
@@ -514,7 +544,8 @@ class Trainer:
         if len(self.dirs) == 1:
             return self.gather("grads")
         gd, gu = self.gather("grads", self.dirs[0]), self.gather("grads", self.dirs[1])
-        return {k: 0.5 * gd[k] if (self.combined_wgrad and k.endswith(GEMM_WEIGHTS)) else 0.5 * (gd[k] + gu[k])
+        combined = {n for s in self.combined_stages for n in self.stage_params[(self.dirs[0], s)].names}
+        return {k: 0.5 * gd[k] if (k in combined and k.endswith(GEMM_WEIGHTS)) else 0.5 * (gd[k] + gu[k])
                 for k in gd}
 
     # ---------------------------------------------------------- introspection --

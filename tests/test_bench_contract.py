@@ -4,6 +4,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -41,3 +43,24 @@ def test_gpus_flag_self_launches_ranks():
     assert len(lines) == 1
     line = json.loads(lines[0])
     assert line["n_gpus"] == 2 and "D=2" in line["config"]["workload"]
+
+
+@pytest.mark.gpu
+def test_multirank_bench_on_one_gpu():
+    """``--gpus 4`` through the self-launcher with every rank on cuda:0
+    (BP_SHARE_GPU=1): the distributed Trainer over the peer transport, the
+    max-over-ranks device timing and the measured multi-rank bubble all run
+    and rank 0 prints one contract line."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    env.update(BP_SHARE_GPU="1", BP_SKIP_CPU_BASELINE="1")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "small", "--gpus", "4",
+                          "--N", "8", "--steps", "2", "--warmup", "3"], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 4 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["transport"].startswith("peer") and "SHARE ONE GPU" in line["transport"]
+    m = line["bubble"]["measured"]
+    assert 0.0 <= m["bubble"] < 1.0 and len(m["busy_ms_per_rank"]) == 4

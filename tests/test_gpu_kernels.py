@@ -455,3 +455,45 @@ def test_gemm_wide_pair_tiles(M, N, K, ak, bk):
     ref = opA @ opB
     assert _relerr(C.float(), ref + bias.float()) < 1e-2
     assert _relerr(C32, base + ref) < 1e-5
+
+
+# -- GPT-10B width (h 4096, 32 heads of 128, s 2048; north-star configs[4]) --
+GPT10B_SHAPES = [
+    # fprop  X[M,K] W[N,K]^T
+    (2048, 12288, 4096, True, True),    # QKV
+    (2048, 4096, 4096, True, True),     # out-projection
+    (2048, 16384, 4096, True, True),    # fc1
+    (2048, 4096, 16384, True, True),    # fc2
+    # dgrad  dY[M,N] W[N,K]  (B MN-major)
+    (2048, 4096, 12288, True, False),   # QKV dgrad
+    (2048, 4096, 16384, True, False),   # fc1 dgrad
+    # deferred wgrad over 16 micro-batch slots: dY^T X, K = 16 M
+    (4096, 4096, 32768, False, False),  # out-projection / fc2-like
+    (16384, 4096, 32768, False, False),  # fc1 weight
+]
+
+
+@pytest.mark.parametrize("M,N,K,ak,bk", GPT10B_SHAPES)
+def test_gemm_gpt10b_width(M, N, K, ak, bk):
+    """tcgen05 2-SM GEMM (auto tiling) at the GPT-10B shapes vs fp32 torch on
+    the same bf16 operands, including fp32 accumulate (beta = 1)."""
+    torch.manual_seed(1)
+    A = (torch.randn(M, K, device="cuda") if ak else torch.randn(K, M, device="cuda")).bfloat16()
+    B = (torch.randn(N, K, device="cuda") if bk else torch.randn(K, N, device="cuda")).bfloat16()
+    opA = A.float() if ak else A.float().t()
+    opB = B.float().t() if bk else B.float()
+    ref = opA @ opB
+    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    ops.gemm(A, B, C, a_kmajor=ak, b_kmajor=bk)
+    torch.cuda.synchronize()
+    assert _relerr(C.float(), ref) < 1e-2
+    C32 = torch.randn(M, N, device="cuda")
+    base = C32.clone()
+    ops.gemm(A, B, C32, a_kmajor=ak, b_kmajor=bk, beta=1.0)
+    torch.cuda.synchronize()
+    assert _relerr(C32, base + ref) < 2e-5 * math.sqrt(K) + 1e-4
+
+
+def test_attention_gpt10b_width():
+    """Causal attention with 32 heads of 128 at s = 2048 (GPT-10B), bf16."""
+    _check_attention(torch.bfloat16, 1, 2048, 32, 128, True)

@@ -218,3 +218,13 @@ def test_without_eager_sync(label):
     device's whole task list -- same step, same numbers."""
     tr = run_pair(label, golden()[label], "tiny", torch.float32, 1e-4, 1e-4, check_params=1e-3, eager_sync=False)
     assert not tr.eager_sync
+
+
+@pytest.mark.parametrize("label", ["D=4;N=8;approach=bitpipe;v=2"])
+def test_partial_deferred_wgrads(label):
+    """Deferred (combined K = N M) weight gradients on some stages only, the
+    per-micro-batch form on the rest -- what the Trainer picks when the
+    slots of every stage do not fit (GPT-10B width)."""
+    tr = run_pair(label, golden()[label], "tiny", torch.float32, 1e-4, 1e-4, check_params=1e-3,
+                  defer_wgrad={0, 3, 5, 6}, expect_combined=True)
+    assert tr.deferred_stages == [0, 3, 5, 6] and tr.combined_stages == {0, 3, 5, 6}

@@ -25,7 +25,16 @@ from oracle.toy_model import ToyModel, toy_run_schedule_numeric, toy_sequential_
 from paper_2410_19367_b200 import schedule as ps
 from paper_2410_19367_b200.model import CONFIGS, init_params, synthetic_batch
 
-torch.set_default_dtype(torch.float64)
+
+
+@pytest.fixture(autouse=True)
+def _float64_default():
+    """float64 tensors by default inside THIS module only (a module-level
+    set_default_dtype would leak into every test collected after it)."""
+    old = torch.get_default_dtype()
+    torch.set_default_dtype(torch.float64)
+    yield
+    torch.set_default_dtype(old)
 
 
 def rel(a, b):
