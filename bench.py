@@ -33,9 +33,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "GPT tokens/sec/box at D=1/2/4/8 B200 (frac of roofline); bubble fraction"
-# ncu --set full, fc1 forward GEMM 2048x8192x2048 (profiles/r1b_ncu_full_summary.txt):
-# dram__bytes_read.sum + dram__bytes_write.sum per launch
-TRAFFIC_FC1_BYTES = 42.101504e6 + 6.494720e6
+# ncu --set full, fc1 forward GEMM 2048x8192x2048 (profiles/r2_ncu_full_summary.txt,
+# round-2 capture, mean of 3 launches): dram__bytes_read.sum + dram__bytes_write.sum per launch
+TRAFFIC_FC1_BYTES = 42.104e6 + 7.097e6
 
 
 def parse():
@@ -431,7 +431,10 @@ def main():
                          "share_of_step": gemm_share, "fc1_fprop_avg_us": fc1_us,
                          "peak_kind": f"{peak_kind} sustained (kernel timed inside a long step)",
                          "traffic_note": "dram read+write bytes per fc1-fprop launch from ncu --set full "
-                                         "(profiles/r1b_ncu_full_summary.txt)"},
+                                         "(profiles/r2_ncu_full_summary.txt); the launch's algorithmic bytes are 109 MB "
+                                         "(X 8 MiB + W 32 MiB read, GELU output + pre-activation 2 x 32 MiB "
+                                         "written): the writes are still in the 126 MB L2 when it ends and "
+                                         "X / W partly hit L2, so DRAM sees less -- no wasted re-reads"},
             "step_roofline": {"tokens_per_s": roof_tps, "frac": value / roof_tps, "F_tok": F_tok,
                               "peak_tflops": peak_sust, "peak_kind": f"{peak_kind} sustained",
                               "beta_ideal": beta_ideal, "model_tflops": value * F_tok / 1e12},

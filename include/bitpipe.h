@@ -89,9 +89,16 @@ enum bp_option {
                                 tile per CTA, 2 two tiles                   */
   BP_OPT_GEMM_OCC = 12,       /* 2-SM GEMM co-resident variant (two CTA pairs
                                 per SM pair, one accumulator, 2 stages):
-                                0 (default) never -- measured slower in the
-                                train step; 1 single-wave launches; 2 always
-                                (tiles <= 256 wide)                         */
+                                0 never; 1 single-wave launches; 2 always
+                                (tiles <= 256 wide); 3 (default) short-K
+                                launches, K <= 1024 (epilogue-dominated:
+                                BERT-large step +3 %; longer main loops need
+                                the deep single-CTA pipeline)               */
+  BP_OPT_GEMM_GRID = 13,      /* 2-SM GEMM grid: 0 (default) one pair per tile
+                                up to all pairs; 1 >= 2 tiles per pair in
+                                equal rounds, leaving SMs to other streams
+                                (measured: GPT-1.3B step 109.0 k vs 109.1 k,
+                                BERT-large +2 %: no default change)          */
 };
 BP_API int bp_set_option(int option, int value);
 

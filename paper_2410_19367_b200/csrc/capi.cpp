@@ -12,7 +12,7 @@ namespace bp {
 
 static thread_local char g_err[1024] = "";
 static std::atomic<unsigned long long> g_launches{0};
-static std::atomic<int> g_opt_attn_exact{0}, g_opt_gemm_simt{0}, g_opt_gemm_mode{0}, g_opt_stream_k{2}, g_opt_gemm_wide{0}, g_opt_gemm_debug{0}, g_opt_gemm_tma_store{1}, g_opt_ln_unfused{0}, g_opt_ln_cps{1}, g_opt_ln_bwd_mode{0}, g_opt_attn_fwd_mode{0}, g_opt_gemm_occ{0};
+static std::atomic<int> g_opt_attn_exact{0}, g_opt_gemm_simt{0}, g_opt_gemm_mode{0}, g_opt_stream_k{2}, g_opt_gemm_wide{0}, g_opt_gemm_debug{0}, g_opt_gemm_tma_store{1}, g_opt_ln_unfused{0}, g_opt_ln_cps{1}, g_opt_ln_bwd_mode{0}, g_opt_attn_fwd_mode{0}, g_opt_gemm_occ{3}, g_opt_gemm_grid{0};
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -53,6 +53,7 @@ int ln_ctas_per_sm() { return g_opt_ln_cps.load(); }
 int ln_bwd_mode() { return g_opt_ln_bwd_mode.load(); }
 int attn_fwd_mode() { return g_opt_attn_fwd_mode.load(); }
 int gemm_occ_mode() { return g_opt_gemm_occ.load(); }
+int gemm_grid_mode() { return g_opt_gemm_grid.load(); }
 
 }  // namespace bp
 
@@ -96,6 +97,7 @@ int bp_set_option(int option, int value) {
     case BP_OPT_LN_BWD_MODE: bp::g_opt_ln_bwd_mode.store(value); return BP_OK;
     case BP_OPT_ATTN_FWD_MODE: bp::g_opt_attn_fwd_mode.store(value); return BP_OK;
     case BP_OPT_GEMM_OCC: bp::g_opt_gemm_occ.store(value); return BP_OK;
+    case BP_OPT_GEMM_GRID: bp::g_opt_gemm_grid.store(value); return BP_OK;
     default: bp::set_error("bp_set_option: unknown option %d", option); return BP_ERR_INVALID;
   }
 }

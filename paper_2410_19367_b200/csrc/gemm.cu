@@ -1086,6 +1086,8 @@ static int sk_workspace(cudaStream_t st, size_t floats, int nflag, SkWs* out) {
   return BP_OK;
 }
 
+int gemm_grid_mode();
+
 template <int BN, bool A_MN, bool B_MN, int OCC>
 static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   using C = Tc2Cfg<BN, B_MN, OCC>;
@@ -1124,6 +1126,15 @@ static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   const int tiles = ((g.M + 255) / 256) * ((g.N + C::BN - 1) / C::BN);
   const int pairs = num_sms() / 2;
   int npairs = tiles < pairs ? tiles : pairs;
+  if (gemm_grid_mode() == 1 && tiles >= 4) {
+    // throughput grid (co-resident executor): at least two tiles per CTA
+    // pair and equal rounds, so every pair overlaps one tile's epilogue with
+    // the next tile's MMAs; the SMs left over run other streams' kernels.
+    // Less SM-time per GEMM than one exposed-epilogue tile per pair.
+    int rounds = (tiles + pairs - 1) / pairs;
+    if (rounds < 2) rounds = 2;
+    npairs = (tiles + rounds - 1) / rounds;
+  }
   SkWs ws{};
   // stream-K: mode 1 = wherever the last wave is ragged; mode 0 (auto) =
   // only sub-wave GEMMs with a long K (>= 64 k-blocks, e.g. the K = 8192
@@ -1186,17 +1197,20 @@ int pick_tc2_bn(int M, int N, int pairs, bool b_mn_major) {
 }
 
 int gemm_occ_mode();
+int gemm_grid_mode();
 
 static int dispatch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   const int pairs = num_sms() / 2;
   const int bn = pick_tc2_bn(g.M, g.N, pairs, !g.b_kmajor);
-  // co-resident variant (BP_OPT_GEMM_OCC: 0 never -- the default, measured
-  // slower: GPT-1.3B step 103.4 k vs 106.7 k tok/s with it on single-wave
-  // launches, its per-launch GEMM time 92 vs 76 us: two 32 KB stages per CTA
-  // do not cover the operand latency; 1 single-wave launches; 2 always)
+  // co-resident variant (BP_OPT_GEMM_OCC: 0 never; 1 single-wave launches;
+  // 2 always; 3 short-K launches, K <= 1024).  Measured: GPT-1.3B step 103.4 k
+  // (mode 1) vs 106.7 k tok/s (0) -- two 32 KB stages per CTA do not cover
+  // the operand latency of K >= 2048 main loops; BERT-large (K = 1024 GEMMs,
+  // epilogue-dominated) 290.0 k (mode 2) vs 278.3 k (0)
   const int occm = gemm_occ_mode();
   const long tiles = (long)((g.M + 255) / 256) * ((g.N + bn - 1) / bn);
-  if (bn <= 256 && occm != 0 && (occm == 2 || tiles <= pairs)) {
+  const bool occ = occm == 2 || (occm == 1 && tiles <= pairs) || (occm == 3 && g.K <= 1024);
+  if (bn <= 256 && occ) {
     switch (bn) {
       case 224: return dispatch_tc2_bn<224, 2>(g, ep, st);
       case 192: return dispatch_tc2_bn<192, 2>(g, ep, st);

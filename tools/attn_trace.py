@@ -34,11 +34,12 @@ print("rc", fn(buf, 1024))
 t = [[buf[i * 16 + k] for k in range(16)] for i in range(64)]
 names = ["q_full", "sdp_full", "tmem_ld", "compute", "mm_done", "st+arr", "->next"]
 print("iter " + " ".join(f"{n:>8s}" for n in names) + " | rel. to iter start: mma_top q_ok sdp_iss dvdk_iss prod_q")
-for i in range(32):
+for i in range(32):   # the traced thread (warp 4) is in compute group 0: even iterations only
     row = t[i]
     if row[0] == 0:
-        break
-    d = [row[k + 1] - row[k] for k in range(6)] + [(t[i + 1][0] - row[6]) if i + 1 < 64 and t[i + 1][0] else 0]
+        continue
+    nxt = t[i + 2][0] if i + 2 < 32 else 0
+    d = [row[k + 1] - row[k] for k in range(6)] + [(nxt - row[6]) if nxt else 0]
     rel = [row[k] - row[0] if row[k] else 0 for k in (8, 9, 10, 11, 12)]
     print(f"{i:4d} " + " ".join(f"{x:8d}" for x in d) + " | " + " ".join(f"{x:8d}" for x in rel))
 
