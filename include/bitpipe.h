@@ -99,6 +99,9 @@ enum bp_option {
                                 equal rounds, leaving SMs to other streams
                                 (measured: GPT-1.3B step 109.0 k vs 109.1 k,
                                 BERT-large +2 %: no default change)          */
+  BP_OPT_GEMM_BN = 14,        /* 2-SM GEMM pair-tile width: 0 (default) the
+                                wave x operand-traffic model, else forced
+                                128 / 192 / 224 / 256 / 512 (measurements)  */
 };
 BP_API int bp_set_option(int option, int value);
 

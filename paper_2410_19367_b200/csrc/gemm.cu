@@ -1170,7 +1170,10 @@ static int dispatch_tc2_bn(const bp_gemm_args& g, const Epi& ep, cudaStream_t st
 // pick the minimum (N = 8192 at M = 2048: 224 gives exactly 4 waves).
 int gemm_wide_mode();
 
+int gemm_force_bn();
+
 int pick_tc2_bn(int M, int N, int pairs, bool b_mn_major) {
+  if (const int f = gemm_force_bn()) return f;   // measurement aid (BP_OPT_GEMM_BN)
   static const int cand[5] = {256, 512, 224, 192, 128};
   const int tm = (M + 255) / 256;
   int best = 256;
