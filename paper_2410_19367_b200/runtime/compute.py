@@ -215,9 +215,11 @@ class StageCompute:
             ops.gemm(S[("logits",)], S[("xf",)], G["head.lm.w"], a_kmajor=False, b_kmajor=False, beta=0.0,
                      stream=q)
 
-    def backward(self, stream, pool: BufferPool, st: Stash, dy, ws, wstream=None):
+    def backward(self, stream, pool: BufferPool, st: Stash, dy, ws, wstream=None, dx_dest=None):
         """Returns (dx0 or None, buffers to release after the task's ``stream``
-        work, buffers also read by side-stream weight-gradient GEMMs)."""
+        work, buffers also read by side-stream weight-gradient GEMMs).
+        ``dx_dest``: where to write the input gradient (the message), e.g.
+        the previous stage's output-gradient slot; else a pool buffer."""
         cfg, P, G = self.cfg, self.sp.p, self.sp.g
         M, h, dt = self.M, cfg.hidden, self.dtype
         H, Dh = cfg.heads, cfg.head_dim
@@ -239,7 +241,8 @@ class StageCompute:
                 wread += [dlogits, xf]
             # gradient w.r.t. the last half-block's output (a wgrad operand
             # slot), or the message when the stage has no half-block
-            dy = self._buf(st, ("dy", hbs[-1]), h, pool, stream) if nhb else pool.get((M, h), dt, stream)
+            dy = self._buf(st, ("dy", hbs[-1]), h, pool, stream) if nhb else \
+                (dx_dest if dx_dest is not None else pool.get((M, h), dt, stream))
             # the LN backward also sums its dx over rows: that is the output-bias
             # gradient of the half-block before it (fused, no separate launch)
             ops.layernorm_bwd(dxf, st.xs[-1], P["head.lnf.w"], mean, rstd, dy, G["head.lnf.w"], G["head.lnf.b"],
@@ -250,8 +253,9 @@ class StageCompute:
             release.append(dy)
             if defer and nhb:  # the incoming message into this micro-batch's output-gradient slot
                 dys = self._buf(st, ("dy", hbs[-1]), h, pool, stream)
-                with torch.cuda.stream(stream):
-                    dys.copy_(dy)
+                if dys.data_ptr() != dy.data_ptr():   # (the co-resident producer wrote it there already)
+                    with torch.cuda.stream(stream):
+                        dys.copy_(dy)
                 dy = dys
             bias_done = self.out_bias_by_next
         for i in range(nhb - 1, -1, -1):
@@ -260,7 +264,8 @@ class StageCompute:
             x = st.xs[i]
             save = st.saves[i]
             # gradient w.r.t. this half-block's input = the previous half-block's output gradient
-            dx = self._buf(st, ("dy", hbs[i - 1]), h, pool, stream) if i > 0 else pool.get((M, h), dt, stream)
+            dx = self._buf(st, ("dy", hbs[i - 1]), h, pool, stream) if i > 0 else \
+                (dx_dest if dx_dest is not None and not self.plan.embed else pool.get((M, h), dt, stream))
             if half == 0:
                 _, a, mean, rstd, qkv, o, lse = save
                 if not defer:

@@ -64,7 +64,7 @@ def issue_order(schedule: Schedule):
     return [(d, i, t) for _, d, i, t in items]
 
 
-def drive(order, num_stages, last_b, *, forward, backward, send, recv, stage_done, dev_of):
+def drive(order, num_stages, last_b, *, forward, backward, send, recv, stage_done, dev_of, stashes=None):
     """Issue every task of ``order`` (list of (device, position, Task)).
 
     Pure host-side control flow shared by the CUDA executor and the
@@ -74,9 +74,11 @@ def drive(order, num_stages, last_b, *, forward, backward, send, recv, stage_don
     stage_done(direction, stage, d, event) fires after the LAST backward of
     that (direction, stage) on device d -- the eager sync launch point.
     Returns the leftover (msgs, stashes), both empty for a valid schedule.
+    ``stashes`` (optional) is the live dict of forward stashes keyed
+    (direction, micro-batch, stage), readable from the callbacks.
     """
     msgs: dict = {}
-    stashes: dict = {}
+    stashes = {} if stashes is None else stashes
     last = num_stages - 1
     for d, i, t in order:
         dr, s, mb = t.direction, t.stage, t.micro_batch
@@ -439,8 +441,8 @@ class Trainer:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
             wst = self.wstreams.get(d)
-            dx, release, release_w = self.compute[(t.direction, t.stage)].backward(stream, self.pool, stash, dy,
-                                                                                 self.ws[d], wstream=wst)
+            dx, release, release_w = self.compute[(t.direction, t.stage)].backward(
+                stream, self.pool, stash, dy, self.ws[d], wstream=wst, dx_dest=self._message_slot(t, live))
             ev = torch.cuda.Event(enable_timing=tl is not None)
             ev.record(stream)
             self.pool.put_all(release, ev, stream)
@@ -454,7 +456,8 @@ class Trainer:
                 tl.append((d, t, e0, done))
             return dx, (ev, done)   # message ready / all of the task's work done
 
-        msgs, stashes = drive(self.order, self.S, self.last_b, forward=forward, backward=backward,
+        live: dict = {}
+        msgs, stashes = drive(self.order, self.S, self.last_b, forward=forward, backward=backward, stashes=live,
                               send=self._send, recv=self._recv,
                               stage_done=(lambda dr, s, d, ev: self._stage_grads_ready(dr, s, d, ev, done_dirs))
                               if self.eager_sync else (lambda *a: deferred_syncs.append(a)),
@@ -490,6 +493,21 @@ class Trainer:
         return StepOutput(self.losses, self.step_count)
 
     # ---------------------------------------------------------------- messages --
+    def _message_slot(self, t, stashes):
+        """Co-resident, deferred weight gradients: the input-gradient message
+        of backward task ``t`` is the previous stage's output-gradient slot
+        of that micro-batch (a weight-gradient GEMM operand), so the producer
+        writes it there directly instead of the consumer copying it in."""
+        if self.dist is not None or t.stage == 0:
+            return None
+        prev = self.compute[(t.direction, t.stage - 1)]
+        if not prev.defer_wgrad or not prev.plan.halfblocks:
+            return None
+        pst = stashes.get((t.direction, t.micro_batch, t.stage - 1))
+        if pst is None:
+            return None
+        return prev._buf(pst, ("dy", prev.plan.halfblocks[-1]), self.cfg.hidden, self.pool, None)
+
     def _send(self, msgs, key, tensor, src, dst, event=None):
         if self.dist is not None and dst != src:
             self.dist.send_msg(self, key, tensor, src, dst)
