@@ -89,11 +89,13 @@ enum bp_option {
                                 tile per CTA, 2 two tiles                   */
   BP_OPT_GEMM_OCC = 12,       /* 2-SM GEMM co-resident variant (two CTA pairs
                                 per SM pair, one accumulator, 2 stages):
-                                0 never; 1 single-wave launches; 2 always
-                                (tiles <= 256 wide); 3 (default) short-K
-                                launches, K <= 1024 (epilogue-dominated:
-                                BERT-large step +3 %; longer main loops need
-                                the deep single-CTA pipeline)               */
+                                0 (default) never; 1 single-wave launches;
+                                2 always (tiles <= 256 wide); 3 short-K
+                                launches (K <= 1024: BERT-large +3 %).  Off
+                                by default: a BERT-large stress run hung
+                                after 1,747 steps with a pair of it stuck
+                                at its first cluster barrier (one CTA never
+                                completed its TMEM allocation)              */
   BP_OPT_GEMM_GRID = 13,      /* 2-SM GEMM grid: 0 (default) one pair per tile
                                 up to all pairs; 1 >= 2 tiles per pair in
                                 equal rounds, leaving SMs to other streams

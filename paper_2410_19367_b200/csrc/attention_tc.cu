@@ -146,19 +146,22 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
   uint64_t* k_empty = bars + 1 + KS;  // [KS]
   uint64_t* v_full = bars + 1 + 2 * KS;   // [2]
   uint64_t* v_empty = v_full + 2;         // [2]
-  uint64_t* s_full = v_full + 4;          // [2]
-  uint64_t* s_free = v_full + 6;          // [2]
-  // P(j) ready: one barrier per j mod 4.  S(j+1) is issued before P V(j), so
-  // a softmax warp can run up to two tiles ahead of a slower one (S(j+2)
-  // only waits for every warp to have READ S(j)); with a single barrier its
-  // arrival for tile j+1 would complete tile j's phase early
-  uint64_t* p_full = v_full + 8;   // [4]
-  uint64_t* pv_done = v_full + 12;
-  uint64_t* o_done = v_full + 13;  // single phase: every P V of the CTA complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_full + 14);
-  // TMEM: S buffers [0,128) and [128,256) (P of tile j is written back as bf16
-  // over the first 64 columns of its S buffer: the TMEM A operand of O += P V),
-  // O [256, 256+Dh)
+  uint64_t* s_full = v_full + 4;          // [3]
+  uint64_t* s_free = v_full + 7;          // [3]
+  // P(j) ready: one barrier per j mod 4.  S(j+2) is issued right after P V(j),
+  // so a softmax warp can run up to three tiles ahead of a slower one (S(j+3)
+  // only waits for every warp to have READ S(j)); with fewer barriers its
+  // arrival for a later tile would complete tile j's phase early
+  uint64_t* p_full = v_full + 10;  // [4]
+  uint64_t* pv_done = v_full + 14;
+  uint64_t* o_done = v_full + 15;  // single phase: every P V of the CTA complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_full + 16);
+  // TMEM: three S buffers [0,128), [128,256), [256,384) -- S(j+2) is computed
+  // while the softmax of tile j runs, so the softmax of tile j+1 never waits
+  // for its scores (with two buffers S(j+1) could only be issued after
+  // P V(j-1), ~300 cycles of every 2,200-cycle tile spent waiting) -- P of
+  // tile j written back as bf16 over the first 64 columns of its S buffer
+  // (the TMEM A operand of O += P V); O [384, 384+Dh)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bh = blockIdx.x, qt = gridDim.y - 1 - blockIdx.y;
@@ -176,6 +179,8 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
     for (int i = 0; i < 2; ++i) {
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 3; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], 256);
     }
@@ -229,34 +234,37 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       const uint32_t aQ = smem_u32(sQ);
       mbar_wait(q_full, 0);
       tc_fence_after();
-      for (int j = 0; j <= n_kv; ++j) {
-        if (j < n_kv) {
-          const int st = j & 1, ks_ = j % KS;
-          mbar_wait(&k_full[ks_], (j / KS) & 1);
-          mbar_wait(&s_free[st], ((j >> 1) & 1) ^ 1);
-          TRACE_MMA(32 + j, 8);
-          tc_fence_after();
-          const uint32_t aK = smem_u32(sK0 + ks_ * C::TILE);
+      auto issue_s = [&](int j) {   // S(j) into buffer j % 3
+        const int sb = j % 3, ks_ = j % KS;
+        mbar_wait(&k_full[ks_], (j / KS) & 1);
+        mbar_wait(&s_free[sb], ((j / 3) & 1) ^ 1);   // every softmax thread has read S(j - 3)
+        TRACE_MMA(32 + j, 8);
+        tc_fence_after();
+        const uint32_t aK = smem_u32(sK0 + ks_ * C::TILE);
 #pragma unroll
-          for (int ks = 0; ks < Dh / 16; ++ks)
-            tc_mma_f16(tmem + st * 128, kdesc(aQ, ks, 128), kdesc(aK, ks, 128), idesc_s, ks > 0);
-          tc_commit(&s_full[st]);
-          tc_commit(&k_empty[ks_]);
-        }
-        if (j >= 1) {
-          const int jj = j - 1, st = jj & 1;
-          mbar_wait(&p_full[jj & 3], (jj >> 2) & 1);
-          mbar_wait(&v_full[st], (jj >> 1) & 1);
-          TRACE_MMA(32 + jj, 9);
-          tc_fence_after();
-          const uint32_t aV = smem_u32(sV0 + st * C::TILE);
+        for (int ks = 0; ks < Dh / 16; ++ks)
+          tc_mma_f16(tmem + sb * 128, kdesc(aQ, ks, 128), kdesc(aK, ks, 128), idesc_s, ks > 0);
+        tc_commit(&s_full[sb]);
+        tc_commit(&k_empty[ks_]);
+      };
+      issue_s(0);
+      if (n_kv > 1) issue_s(1);
+      for (int jj = 0; jj < n_kv; ++jj) {
+        const int vs = jj & 1;
+        mbar_wait(&p_full[jj & 3], (jj >> 2) & 1);
+        mbar_wait(&v_full[vs], (jj >> 1) & 1);
+        TRACE_MMA(32 + jj, 9);
+        tc_fence_after();
+        const uint32_t aV = smem_u32(sV0 + vs * C::TILE);
 #pragma unroll
-          for (int ks = 0; ks < 8; ++ks)
-            tc_mma_f16_ts(tmem + 256, tmem + st * 128 + 8 * ks, mndesc(aV, ks, 128), idesc_o, (jj > 0 || ks > 0));
-          tc_commit(pv_done);
-          tc_commit(&v_empty[st]);
-          if (jj == n_kv - 1) tc_commit(o_done);
-        }
+        for (int ks = 0; ks < 8; ++ks)
+          tc_mma_f16_ts(tmem + 384, tmem + (jj % 3) * 128 + 8 * ks, mndesc(aV, ks, 128), idesc_o, (jj > 0 || ks > 0));
+        tc_commit(pv_done);
+        tc_commit(&v_empty[vs]);
+        if (jj == n_kv - 1) tc_commit(o_done);
+        // after P V(jj) in the in-order tensor pipe: S(jj + 2) overwrites the
+        // buffer of P(jj - 1), which P V(jj - 1) has consumed
+        if (jj + 2 < n_kv) issue_s(jj + 2);
       }
     }
   } else if (warp >= 4) {  // ---------------------------------- softmax
@@ -266,9 +274,9 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
     constexpr int OC = Dh / 64;  // 32-column O chunks per half
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < n_kv; ++j) {
-      const int st = j & 1;
+      const int st = j % 3;
       TRACE(32 + j, 0);
-      mbar_wait(&s_full[st], (j >> 1) & 1);
+      mbar_wait(&s_full[st], (j / 3) & 1);
       TRACE(32 + j, 1);
       tc_fence_after();
       float s[64];
@@ -311,7 +319,7 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
 #pragma unroll 1
         for (int c = 0; c < OC; ++c) {
           float ov[32];
-          const uint32_t ta = tl + 256 + (hh * OC + c) * 32;
+          const uint32_t ta = tl + 384 + (hh * OC + c) * 32;
           tmem_ld_32x32b_x32(ta, ov);
 #pragma unroll
           for (int i = 0; i < 32; ++i) ov[i] *= f;
@@ -359,7 +367,7 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
 #pragma unroll 1
     for (int c = hh * OC; c < (hh + 1) * OC; ++c) {
       float ov[32];
-      tmem_ld_32x32b_x32(tl + 256 + c * 32, ov);
+      tmem_ld_32x32b_x32(tl + 384 + c * 32, ov);
 #pragma unroll
       for (int i = 0; i < 32; ++i) ov[i] *= inv;
 #pragma unroll

@@ -12,7 +12,7 @@ namespace bp {
 
 static thread_local char g_err[1024] = "";
 static std::atomic<unsigned long long> g_launches{0};
-static std::atomic<int> g_opt_attn_exact{0}, g_opt_gemm_simt{0}, g_opt_gemm_mode{0}, g_opt_stream_k{2}, g_opt_gemm_wide{0}, g_opt_gemm_debug{0}, g_opt_gemm_tma_store{1}, g_opt_ln_unfused{0}, g_opt_ln_cps{1}, g_opt_ln_bwd_mode{0}, g_opt_attn_fwd_mode{0}, g_opt_gemm_occ{3}, g_opt_gemm_grid{0}, g_opt_gemm_bn{0};
+static std::atomic<int> g_opt_attn_exact{0}, g_opt_gemm_simt{0}, g_opt_gemm_mode{0}, g_opt_stream_k{2}, g_opt_gemm_wide{0}, g_opt_gemm_debug{0}, g_opt_gemm_tma_store{1}, g_opt_ln_unfused{0}, g_opt_ln_cps{1}, g_opt_ln_bwd_mode{0}, g_opt_attn_fwd_mode{0}, g_opt_gemm_occ{0}, g_opt_gemm_grid{0}, g_opt_gemm_bn{0};
 
 void set_error(const char* fmt, ...) {
   va_list ap;

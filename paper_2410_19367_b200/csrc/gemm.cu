@@ -1205,11 +1205,14 @@ int gemm_grid_mode();
 static int dispatch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   const int pairs = num_sms() / 2;
   const int bn = pick_tc2_bn(g.M, g.N, pairs, !g.b_kmajor);
-  // co-resident variant (BP_OPT_GEMM_OCC: 0 never; 1 single-wave launches;
-  // 2 always; 3 short-K launches, K <= 1024).  Measured: GPT-1.3B step 103.4 k
-  // (mode 1) vs 106.7 k tok/s (0) -- two 32 KB stages per CTA do not cover
-  // the operand latency of K >= 2048 main loops; BERT-large (K = 1024 GEMMs,
-  // epilogue-dominated) 290.0 k (mode 2) vs 278.3 k (0)
+  // co-resident variant (BP_OPT_GEMM_OCC: 0 never -- the default; 1
+  // single-wave launches; 2 always; 3 short-K launches, K <= 1024).
+  // Measured: GPT-1.3B step 103.4 k (mode 1) vs 106.7 k tok/s (0) -- two
+  // 32 KB stages per CTA do not cover the operand latency of K >= 2048 main
+  // loops; BERT-large (K = 1024 GEMMs, epilogue-dominated) 290.0 k (mode 2),
+  // 286.3 k (3) vs 278.3 k (0), but a BERT-large stress run with mode 3 hung
+  // after 1,747 steps (a CTA pair of this variant at its first cluster
+  // barrier, one CTA never through its TMEM allocation): not the default
   const int occm = gemm_occ_mode();
   const long tiles = (long)((g.M + 255) / 256) * ((g.N + bn - 1) / bn);
   const bool occ = occm == 2 || (occm == 1 && tiles <= pairs) || (occm == 3 && g.K <= 1024);
