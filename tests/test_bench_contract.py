@@ -64,3 +64,24 @@ def test_multirank_bench_on_one_gpu():
     assert line["transport"].startswith("peer") and "SHARE ONE GPU" in line["transport"]
     m = line["bubble"]["measured"]
     assert 0.0 <= m["bubble"] < 1.0 and len(m["busy_ms_per_rank"]) == 4
+
+
+@pytest.mark.gpu
+def test_single_gpu_bench_line():
+    """``bench.py`` (our arm, N = 1) on a small configuration: the contract
+    keys, the roofline / cpu_baseline / e2e / clocks objects and a positive
+    native launch count."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "small", "--D", "4", "--N", "8",
+                          "--steps", "3", "--warmup", "3"], capture_output=True, text=True, timeout=600, cwd=ROOT,
+                         env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "e2e", "roofline", "cpu_baseline", "gpu_launches", "clocks"):
+        assert k in line, k
+    assert line["n_gpus"] == 1 and line["steps"] == 3 and line["warmup"] == 3 and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
+    assert line["roofline"]["unit"] == "TFLOP/s" and 0 < line["roofline"]["frac"] < 1.2
+    assert line["cpu_baseline"]["cores"] >= 1 and line["gpu_launches"] > 0
+    assert "workload" in line["config"]
