@@ -299,8 +299,8 @@ __device__ long long g_gemm_etrace[2 * 160][8][5];  // first tile, epilogue warp
 
 // Per-warp state of the TMA epilogue, carried across tiles.
 struct EpiTma {
-  uint8_t* stage;    // 2 units x 4 KB: [0, 2K) output / [2K, 4K) aux-out or input
-  uint64_t* bar;     // 2 mbarriers (input tile landed in unit u)
+  uint8_t* stage;    // U units x 4 KB: [0, 2K) output / [2K, 4K) aux-out or input
+  uint64_t* bar;     // U mbarriers (input tile landed in unit u)
   int ubuf;          // next unit
   uint32_t phase;    // bit u = parity of bar[u]
 };
@@ -315,7 +315,9 @@ BP_DEV void epi_tma_prefetch_input(const CUtensorMap* mx, EpiTma& es, int u, int
   tma_load_2d(dst, mx, c0, row0, &es.bar[u]);
 }
 
-template <int NCHUNK>
+// U staging units per epilogue warp: up to U - 1 TMA stores of earlier
+// chunks may still be reading shared memory while chunk c is staged.
+template <int NCHUNK, int U = 2>
 BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap* mx, uint32_t tmem_addr,
                          int row0, int lane, int n0, EpiTma& es, bool input_issued, bool etr = false,
                          const float* sbias = nullptr) {
@@ -329,7 +331,7 @@ BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap
     const int u = es.ubuf;
     uint8_t* unit = es.stage + u * 4096;
     if (has_in && lane == 0 && c + 1 < NCHUNK && c0 + 32 < ep.N)
-      epi_tma_prefetch_input(mx, es, u ^ 1, c0 + 32, row0);
+      epi_tma_prefetch_input(mx, es, (u + 1) % U, c0 + 32, row0);
     ETRACE(c, 0);
     float v[32];
     tmem_ld_32x32b_x32(tmem_addr + c * 32, v);
@@ -363,7 +365,7 @@ BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap
         for (int i = 0; i < 32; ++i) v[i] += cur[i];
       }
     }
-    if (lane == 0) bulk_wait_read<1>();  // this unit's previous store has read it
+    if (lane == 0) bulk_wait_read<U - 1>();  // this unit's previous store has read it
     __syncwarp();
     ETRACE(c, 3);
     if (gelu) {
@@ -395,7 +397,7 @@ BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap
       bulk_commit();
     }
     ETRACE(c, 4);
-    es.ubuf ^= 1;
+    es.ubuf = (es.ubuf + 1) % U;
   }
 }
 
@@ -642,19 +644,25 @@ struct Tc2Cfg {
   static constexpr uint32_t A_BYTES = BM * BK * 2;
   static constexpr uint32_t SUB_BYTES = B_MN_ ? BCH * 64 * BK * 2 : SUBH * BK * 2;
   static constexpr uint32_t B_BYTES = NSUB * SUB_BYTES;
-  static constexpr uint32_t EPI_BYTES = 4 * 2 * 4096;  // 2 TMA-store staging units per epilogue warp
-  static constexpr uint32_t BIAS_BYTES = 4 * BN_;       // the tile's bias columns (fp32)
   static constexpr int OCC = OCC_;
+  // TMA-store staging units per epilogue warp (up to EPI_UNITS - 1 earlier
+  // chunks' stores in flight).  Measured with 4: single-tile epilogues no
+  // faster (proj fprop 27.7 us either way) and the stage lost to the extra
+  // 32 KB slows the long-K launches (fc2 fprop 58.4 -> 60.4 us)
+  static constexpr int EPI_UNITS = 2;
+  static constexpr uint32_t EPI_BYTES = 4 * EPI_UNITS * 4096;
+  static constexpr uint32_t BIAS_BYTES = 4 * BN_;       // the tile's bias columns (fp32)
   static_assert(OCC == 1 || (OCC == 2 && BN_ <= 256), "co-resident variant: one <= 256-column accumulator");
   // per-CTA budget: the SM's 232448 B (OCC = 1), or half of it less the
   // 1 KB the hardware reserves per resident CTA (OCC = 2)
   static constexpr int SM_BUDGET = OCC == 1 ? 232448 : 232448 / 2 - 1024;
-  static constexpr int STAGE_BUDGET = SM_BUDGET - 1024 - 256 - (int)EPI_BYTES - (int)BIAS_BYTES;
+  static constexpr int STAGE_BUDGET = SM_BUDGET - 1024 - 512 - (int)EPI_BYTES - (int)BIAS_BYTES;
   static constexpr int STAGES = STAGE_BUDGET / (A_BYTES + B_BYTES) > 8 ? 8 : STAGE_BUDGET / (A_BYTES + B_BYTES);
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int ACC = (OCC == 1 && 2 * BN_ <= 512) ? 2 : 1;  // TMEM accumulator buffers
   static constexpr uint32_t TMEM_COLS = ACC * BN_ <= 256 ? 256 : 512;  // power of two
-  static constexpr size_t SMEM = 1024 + STAGES * (size_t)STAGE_BYTES + EPI_BYTES + BIAS_BYTES + 256;
+  static constexpr size_t SMEM = 1024 + STAGES * (size_t)STAGE_BYTES + EPI_BYTES + BIAS_BYTES + 512;  // 512 B barriers
+  static_assert((2 * STAGES + 4 + 4 * EPI_UNITS) * 8 + 4 <= 512, "barrier region");
 };
 
 template <int BN, bool A_MN, bool B_MN, int OCC>
@@ -674,8 +682,8 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* ebar = tempty + 2;  // 4 epilogue warps x 2 input-tile barriers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 8);
+  uint64_t* ebar = tempty + 2;  // 4 epilogue warps x EPI_UNITS input-tile barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 4 * C::EPI_UNITS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -710,7 +718,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 256);
     }
-    for (int e = 0; e < 8; ++e) mbar_init(&ebar[e], 1);
+    for (int e = 0; e < 4 * C::EPI_UNITS; ++e) mbar_init(&ebar[e], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_2sm<C::TMEM_COLS>(tmem_slot);
@@ -801,7 +809,7 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   } else if (warp >= 4) {  // ---------------------- epilogue (both CTAs)
     const int ew = warp - 4;
     int it = 0;
-    EpiTma es{sEpi + ew * 8192, ebar + 2 * ew, 0, 0u};
+    EpiTma es{sEpi + ew * C::EPI_UNITS * 4096, ebar + C::EPI_UNITS * ew, 0, 0u};
     const bool tma_in = ep.tma_store && (ep.residual != nullptr || ep.epilogue == BP_EPI_DGELU);
     if (ep.tma_store && lane == 0) {
       tma_prefetch_desc(&map_c);
@@ -880,7 +888,8 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           if (n0 + c * 32 < N) epi_row32(ep, row, n0 + c * 32, v);
         }
       } else if (ep.tma_store) {
-        epi_tile_tma<C::BN / 32>(ep, &map_c, &map_aux, t0, m0 + ew * 32, lane, n0, es, tma_in, si == 0 && ew == 0,
+        epi_tile_tma<C::BN / 32, C::EPI_UNITS>(ep, &map_c, &map_aux, t0, m0 + ew * 32, lane, n0, es, tma_in,
+                                              si == 0 && ew == 0,
                                  sbias ? sBias : nullptr);
       } else {
         epi_tile<C::BN / 32>(ep, t0, row, n0);
