@@ -2,15 +2,15 @@
 float64 CPU oracle (run once in the build container; the GPU box only reads
 the committed ``numeric_*.pt``).  See ``numeric.py`` for what is stored.
 
-Each case: the reduced-depth model at full width, BitPipe D=4 N=8 with the
-F2 paper-gate order (gate stage 3) and the cost-balanced partition, seeded
+Each case (``numeric.case_specs``): the reduced-depth model at full width,
+BitPipe with the F2 paper-gate order and the cost-balanced partition, seeded
 parameters (``init_params(cfg, 7, perturb=True)``) and tokens
-(``synthetic_batch(cfg, 8, seed=11)``), AdamW lr 1e-3 wd 0.01.  The oracle
+(``synthetic_batch(cfg, N, seed=11)``), AdamW lr 1e-3 wd 0.01.  The oracle
 executes the reference-format dump of that order with message passing
 (SPEC run_schedule_numeric); schedule independence of that executor is
 tested separately (tests/test_oracle.py, tests/test_oracle_pinning.py).
 
-Usage:  python tests/golden/make_numeric_golden.py [case ...]   (~10 min for GPT)
+Usage:  python tests/golden/make_numeric_golden.py [case ...]   (~1-5 min per case)
 """
 from __future__ import annotations
 

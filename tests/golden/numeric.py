@@ -31,12 +31,15 @@ PARAM_SEED, DATA_SEED = 7, 11
 
 
 def case_specs():
-    """name -> (base config, layers, D, N, paper-policy order, partition)."""
+    """name -> (base config, layers, D, N): BitPipe with the paper-policy
+    order and the cost-balanced partition."""
     return {
         # GPT-1.3B width: h 2048, 16 heads of 128, s 2048, V 50304, causal
         "gpt-1.3b-L4": ("gpt-1.3b", 4, 4, 8),
         # BERT-large width: h 1024, 16 heads of 64, s 512, B 4, V 30528, bidirectional
         "bert-large-L4": ("bert-large", 4, 4, 8),
+        # GPT-10B width: h 4096, 32 heads of 128, s 2048, V 50304, causal (one layer)
+        "gpt-10b-L1": ("gpt-10b", 1, 2, 4),
     }
 
 
