@@ -40,7 +40,7 @@ from . import ops
 from .compute import StageCompute
 from .state import GEMM_WEIGHTS, BufferPool, StageParams
 
-__all__ = ["Trainer", "StepOutput", "issue_order", "drive"]
+__all__ = ["Trainer", "StepOutput", "issue_order", "drive", "choose_deferred_stages"]
 
 
 @dataclass
@@ -62,6 +62,22 @@ def issue_order(schedule: Schedule):
             items.append((starts[t], d, i, t))
     items.sort(key=lambda x: (x[0], x[1], x[2]))
     return [(d, i, t) for _, d, i, t in items]
+
+
+def choose_deferred_stages(slot_bytes: dict, work: dict, budget: float) -> set:
+    """Stages whose weight gradients are deferred: all of them when their
+    slots fit ``budget`` bytes, else greedily the stages with the most
+    weight-GEMM work per slot byte (ties: lower stage first) while they fit;
+    the rest keep per-micro-batch weight gradients.  So a model too large for
+    every slot (e.g. the GPT-10B width) still defers most of its GEMMs."""
+    if sum(slot_bytes.values()) <= budget:
+        return set(slot_bytes)
+    chosen, used = set(), 0
+    for s in sorted(slot_bytes, key=lambda s: (-work[s] / max(1, slot_bytes[s]), s)):
+        if slot_bytes[s] and used + slot_bytes[s] <= budget:
+            chosen.add(s)
+            used += slot_bytes[s]
+    return chosen
 
 
 def drive(order, num_stages, last_b, *, forward, backward, send, recv, stage_done, dev_of, stashes=None):
@@ -288,25 +304,15 @@ class Trainer:
 
     def _deferred_stages(self, dtype, budget: float) -> set:
         """Stages whose weight gradients are deferred to one K = N M GEMM per
-        weight: all of them when their slots fit ``budget`` bytes, else the
-        stages with the most weight-GEMM work per slot byte first (the
-        per-micro-batch form stays for the rest) -- so a model too large for
-        all slots (e.g. the GPT-10B width) still defers most of its GEMMs."""
-        sizes = {s: self._slot_bytes(dtype, s) for s in range(self.S)}
-        if sum(sizes.values()) <= budget:
-            return set(range(self.S))
+        weight (``choose_deferred_stages`` over this process's slot sizes)."""
         cfg = self.cfg
 
         def work(s):   # weight-gradient FLOPs per micro-batch token of stage s
             w = sum(8 * cfg.hidden ** 2 if hb % 2 == 0 else 2 * cfg.hidden * cfg.ffn for hb in self.plans[s].halfblocks)
             return w + (cfg.hidden * cfg.vocab if self.plans[s].head else 0)
 
-        chosen, used = set(), 0
-        for s in sorted(range(self.S), key=lambda s: (-work(s) / max(1, sizes[s]), s)):
-            if sizes[s] and used + sizes[s] <= budget:
-                chosen.add(s)
-                used += sizes[s]
-        return chosen
+        return choose_deferred_stages({s: self._slot_bytes(dtype, s) for s in range(self.S)},
+                                      {s: work(s) for s in range(self.S)}, budget)
 
     def _stream_priorities(self, mode) -> dict:
         """Co-resident CUDA stream priorities (lower = more urgent).  'tail':
