@@ -104,6 +104,10 @@ enum bp_option {
   BP_OPT_GEMM_BN = 14,        /* 2-SM GEMM pair-tile width: 0 (default) the
                                 wave x operand-traffic model, else forced
                                 128 / 192 / 224 / 256 / 512 (measurements)  */
+  BP_OPT_ATTN_BWD_MODE = 15,  /* tcgen05 attention backward: 0 (default) the
+                                dK/dV kernel stores dS^T (bf16, in the
+                                workspace) and dQ = dS K runs as a GEMM over
+                                it; 1 the dQ kernel recomputes S and dP     */
 };
 BP_API int bp_set_option(int option, int value);
 

@@ -193,9 +193,17 @@ static int bwd_exact(int B, int S, int H, int Dh, int causal, float scale, const
 
 using namespace bp;
 
+namespace bp {
+// tcgen05 backward: dS^T (bf16 [B H][S][S]) after delta, 256-byte aligned
+int64_t attn_ds_offset_floats(int B, int S, int H) { return ((int64_t)B * H * S + 63) / 64 * 64; }
+}
+
 extern "C" int64_t bp_attn_workspace_bytes(int B, int S, int H, int Dh) {
-  // delta [B*H*S] + three fp32 [B*S, H*Dh] accumulators (dq/dk/dv)
-  return (int64_t)sizeof(float) * ((int64_t)B * H * S + 3LL * B * S * H * Dh);
+  // delta [B*H*S] + three fp32 [B*S, H*Dh] accumulators (dq/dk/dv, exact
+  // path), or delta + the bf16 dS^T matrix of the tcgen05 path
+  const int64_t exact = (int64_t)sizeof(float) * ((int64_t)B * H * S + 3LL * B * S * H * Dh);
+  const int64_t tc = (int64_t)sizeof(float) * attn_ds_offset_floats(B, S, H) + 2LL * B * H * S * S;
+  return exact > tc ? exact : tc;
 }
 
 static int attn_check(int B, int S, int H, int Dh) {

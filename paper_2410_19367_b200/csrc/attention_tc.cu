@@ -29,6 +29,8 @@ void count_launch();
 int num_sms();
 bool opt_attn_no_tc();
 int attn_fwd_mode();
+int attn_bwd_mode();
+int64_t attn_ds_offset_floats(int B, int S, int H);
 int make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, int64_t ld, uint32_t box_inner,
              uint32_t box_outer);
 
@@ -647,7 +649,8 @@ template <int Dh, bool CAUSAL>
 __global__ void __launch_bounds__(384, 1)
 dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUtensorMap map_q,
         const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse, const float* __restrict__ delta,
-        __nv_bfloat16* __restrict__ dqkv, float* __restrict__ dbias, int S, int H, float scale, float scale_log2) {
+        __nv_bfloat16* __restrict__ dqkv, float* __restrict__ dbias, int S, int H, float scale, float scale_log2,
+        __nv_bfloat16* __restrict__ ds_t) {
   using C = Dkdv<Dh>;
   constexpr int QST = C::QST;
   extern __shared__ uint8_t smem_raw[];
@@ -833,6 +836,11 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
         }
         tmem_st_32x32b_x16(tl + hf * 16, pk);
         tmem_st_32x32b_x16(tl + 64 + hf * 16, dk);
+        if (ds_t) {  // dS^T row of this key, 32 queries (64 B), for the dQ GEMM
+          uint4* dst = reinterpret_cast<uint4*>(ds_t + ((int64_t)bh * S + key) * S + qi * 64 + hf * 32);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dst[u] = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+        }
         TRACE(it, 5);
       }
       tmem_wait_st();
@@ -1065,6 +1073,120 @@ dq_tc(const __grid_constant__ CUtensorMap map_q128, const __grid_constant__ CUte
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+
+// ===================================================== backward: dQ from dS ====
+// dQ = scale dS K as a plain tcgen05 GEMM over the dS^T tiles the dK/dV
+// kernel stored (bf16 [B H][S keys][S queries], exactly the values it used
+// for dK): no recomputation of S = Q K^T and dP = dO V^T (7 -> 5 attention
+// GEMMs).  CTA = 128 queries of one (batch, head); warp 0 TMA producer, warp
+// 1 MMA issuer, warp 2 TMEM allocator, warps 4-7 epilogue.  Per 64-key tile:
+// A = dS (M = 128 queries, K = 64 keys; the dS^T tile is its MN-major
+// storage), B = K (K = 64 keys, N = Dh; MN-major), D = dQ in TMEM.
+template <int Dh>
+struct DqDs {
+  static constexpr int DC = Dh / 64;
+  static constexpr int ST = 6;
+  static constexpr uint32_t AT = 64 * 128 * 2;   // dS^T tile: 64 keys x 128 queries
+  static constexpr uint32_t BT = 64 * Dh * 2;    // K tile: 64 keys x Dh
+  static constexpr size_t SMEM = 1024 + ST * (AT + BT) + 256;
+};
+
+template <int Dh, bool CAUSAL>
+__global__ void __launch_bounds__(256, 1)
+dq_ds_tc(const __grid_constant__ CUtensorMap map_ds, const __grid_constant__ CUtensorMap map_kv64,
+         __nv_bfloat16* __restrict__ dqkv, float* __restrict__ dbias, int S, int H, float scale) {
+  using C = DqDs<Dh>;
+  constexpr int ST = C::ST;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA0 = smem;                      // stage s: dS^T at sA0 + s AT
+  uint8_t* sB0 = smem + ST * C::AT;         // stage s: K at sB0 + s BT
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB0 + ST * C::BT);
+  uint64_t* empty = full + ST;
+  uint64_t* done = empty + ST;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bh = blockIdx.x, qt = gridDim.y - 1 - blockIdx.y;
+  const int b = bh / H, h = bh % H;
+  const int n_it = CAUSAL ? 2 * qt + 2 : S / 64;
+  const int HD = H * Dh;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_ds);
+    tma_prefetch_desc(&map_kv64);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<Dh>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------ producer
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it % ST;
+        mbar_wait(&empty[st], ((it / ST) & 1) ^ 1);
+        const int kr = it * 64;
+        // dS^T rows (bh S + keys), query columns in two 64-wide boxes
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d(sA0 + st * C::AT + c * 8192, &map_ds, qt * 128 + c * 64, bh * S + kr, &full[st]);
+#pragma unroll
+        for (int c = 0; c < C::DC; ++c)
+          tma_load_2d(sB0 + st * C::BT + c * 8192, &map_kv64, HD + h * Dh + c * 64, b * S + kr, &full[st]);
+        mbar_expect_tx(&full[st], C::AT + C::BT);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------ MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(128, Dh, true, true);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it % ST;
+        mbar_wait(&full[st], (it / ST) & 1);
+        tc_fence_after();
+        const uint32_t aA = smem_u32(sA0 + st * C::AT), aB = smem_u32(sB0 + st * C::BT);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)  // 64 keys / 16
+          tc_mma_f16(tmem, mndesc(aA, ks, 64), mndesc(aB, ks, 64), idesc, (it > 0 || ks > 0));
+        tc_commit(&empty[st]);
+      }
+      tc_commit(done);
+    }
+  } else if (warp >= 4) {  // ---------------------------------- epilogue
+    const int wq = warp & 3;
+    const int q = qt * 128 + wq * 32 + lane;
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const uint32_t te = tmem + ((uint32_t)(wq * 32) << 16);
+    __nv_bfloat16* dqrow = dqkv + ((int64_t)b * S + q) * 3 * HD + h * Dh;
+#pragma unroll 1
+    for (int c = 0; c < Dh / 32; ++c) {
+      float v[32];
+      tmem_ld_32x32b_x32(te + c * 32, v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] *= scale;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(dqrow + c * 32 + 8 * u) = pack8(v + 8 * u);
+      if (dbias) {  // Q-bias gradient: column sums of this warp's 32 queries, as stored
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = bf16_round(v[i]);
+        atomicAdd(dbias + h * Dh + c * 32 + lane, warp_colsum32(v, lane));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<Dh>(tmem);
+}
+
 // delta[b,h,i] = <O[b,i,h,:], dO[b,i,h,:]>: Dh/8 lanes per (token, head)
 // row, one 16-byte load of O and dO per lane, rows in memory order.
 template <int Dh>
@@ -1152,18 +1274,30 @@ static int bwd(int B, int S, int H, float scale, float* dbias, const void* qkv, 
   if (int rc = make_map(&do128, dout, (uint64_t)H * Dh, R, (int64_t)H * Dh, 64, 128)) return rc;
   auto k1 = dkdv_tc<Dh, CAUSAL>;
   auto k2 = dq_tc<Dh, CAUSAL>;
+  auto k3 = dq_ds_tc<Dh, CAUSAL>;
   static bool once = false;
   if (!once) {
     if (int rc = set_smem(k1, Dkdv<Dh>::SMEM)) return rc;
     if (int rc = set_smem(k2, Dq<Dh>::SMEM)) return rc;
+    if (int rc = set_smem(k3, DqDs<Dh>::SMEM)) return rc;
     once = true;
   }
   const float sl2 = scale * kLog2e;
+  // mode 0 (default): dK/dV stores dS^T, dQ = dS K as a GEMM over it; mode 1:
+  // the dQ kernel recomputes S and dP
+  const bool via_ds = attn_bwd_mode() == 0;
+  __nv_bfloat16* ds_t = via_ds ? reinterpret_cast<__nv_bfloat16*>(ws + attn_ds_offset_floats(B, S, H)) : nullptr;
   k1<<<dim3(B * H, S / 128), 384, Dkdv<Dh>::SMEM, st>>>(kv128, q64, do64, lse, delta, (__nv_bfloat16*)dqkv, dbias, S, H,
-                                                         scale, sl2);
+                                                         scale, sl2, ds_t);
   count_launch();
-  k2<<<dim3(B * H, S / 128), 384, Dq<Dh>::SMEM, st>>>(q128, kv64, do128, lse, delta, (__nv_bfloat16*)dqkv, dbias, S, H,
-                                                       scale, sl2);
+  if (via_ds) {
+    CUtensorMap mds;
+    if (int rc = make_map(&mds, ds_t, (uint64_t)S, (uint64_t)B * H * S, (int64_t)S, 64, 64)) return rc;
+    k3<<<dim3(B * H, S / 128), 256, DqDs<Dh>::SMEM, st>>>(mds, kv64, (__nv_bfloat16*)dqkv, dbias, S, H, scale);
+  } else {
+    k2<<<dim3(B * H, S / 128), 384, Dq<Dh>::SMEM, st>>>(q128, kv64, do128, lse, delta, (__nv_bfloat16*)dqkv, dbias, S,
+                                                         H, scale, sl2);
+  }
   count_launch();
   BP_CHECK_LAUNCH("attn_bwd_tc");
   return BP_OK;
