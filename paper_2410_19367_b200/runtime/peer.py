@@ -160,8 +160,15 @@ class PeerContext(DistContext):
         if len({i["host"] for i in infos}) != 1:
             raise RuntimeError("peer transport: all ranks must run on one node (CUDA IPC, shared memory)")
         if self.rank != 0:
-            self._shm = shared_memory.SharedMemory(name=infos[0]["shm"])
-            resource_tracker.unregister(self._shm._name, "shared_memory")   # rank 0 owns (and unlinks) it
+            # attach WITHOUT registering with the resource tracker (Python 3.12
+            # registers attaches too, and would unlink rank 0's segment when
+            # this process exits); rank 0 owns and unlinks it
+            reg = resource_tracker.register
+            resource_tracker.register = lambda *a, **k: None
+            try:
+                self._shm = shared_memory.SharedMemory(name=infos[0]["shm"])
+            finally:
+                resource_tracker.register = reg
         self.cnt = np.ndarray((n_counters,), dtype=np.int64, buffer=self._shm.buf)
         if self.rank == 0:
             self.cnt[:] = 0
