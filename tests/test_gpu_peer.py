@@ -153,7 +153,13 @@ def test_peer_transport_train_step(label, world, cfg_name, dtype_name, tol):
         master = {}
         for r in results:
             master.update(r["master"])
-        werr = {k: rel(master[k] - params[k], ref1.params[k] - params[k].double()) for k in params}
+        # the first AdamW step is ~sign(g): compare where the oracle gradient
+        # is not negligible (see tests/test_gpu_train_step.run_pair)
+        werr = {}
+        for k in params:
+            gr = ref1.grads[k].double()
+            m = gr.abs() > 0.05 * gr.pow(2).mean().sqrt()
+            werr[k] = rel((master[k] - params[k])[m], (ref1.params[k] - params[k].double())[m]) if m.any() else 0.0
         wk = max(werr, key=werr.get)
         assert werr[wk] < 1e-3, (wk, werr[wk])
 

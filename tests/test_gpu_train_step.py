@@ -83,10 +83,25 @@ def run_pair(label, text, cfg_name, dtype, tol_loss, tol_grad, check_params, par
     wk = max(errs, key=errs.get)
     assert errs[wk] < tol_grad, (wk, errs[wk], ref.grads[wk].norm().item())
     if check_params:
+        # The first AdamW step is ~sign(g) per element: wherever the exact
+        # gradient is ~0 (e.g. the key bias, exactly 0 by softmax shift
+        # invariance) its sign -- and so the update -- is rounding noise in
+        # both implementations, and the fp32 atomics make that noise differ
+        # run to run.  So compare the update (i) with AdamW applied to OUR
+        # gradient, everywhere, and (ii) with the oracle's update on the
+        # elements whose oracle gradient is not negligible (> 5 % of the
+        # tensor's RMS gradient).
+        from tests.golden.numeric import adamw_first_step
         master = tr.gather("master")
-        upd_ours = {k: master[k] - params[k] for k in params}
-        upd_ref = {k: ref.params[k] - params[k].double() for k in params}
-        werrs = {k: rel(upd_ours[k], upd_ref[k]) for k in params}
+        upd_ours = {k: master[k].double() - params[k].double() for k in params}
+        own = {k: rel(upd_ours[k], adamw_first_step(params[k], grads[k], opt)) for k in params}
+        wk = max(own, key=own.get)
+        assert own[wk] < 1e-4, (wk, own[wk])
+        werrs = {}
+        for k in params:
+            gr = ref.grads[k].double()
+            mask = gr.abs() > 0.05 * gr.pow(2).mean().sqrt()
+            werrs[k] = rel(upd_ours[k][mask], (ref.params[k] - params[k].double())[mask]) if mask.any() else 0.0
         wk = max(werrs, key=werrs.get)
         assert werrs[wk] < check_params, (wk, werrs[wk])
         # both replicas hold bit-identical working weights after the update
