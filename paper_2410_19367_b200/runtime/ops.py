@@ -170,6 +170,9 @@ def attn_bwd(qkv, o, dout, lse, dqkv, workspace, B, S, H, Dh, causal, scale, str
     (the QKV bias gradient, fused into the tcgen05 kernels)."""
     if dbias is not None and (dbias.dtype != torch.float32 or dbias.numel() != 3 * H * Dh):
         raise ValueError("dbias must be an fp32 [3*H*Dh] tensor")
+    need = attn_workspace_numel(B, S, H, Dh)
+    if workspace.dtype != torch.float32 or workspace.numel() < need:
+        raise ValueError(f"attention workspace must be fp32 with >= {need} elements (attn_workspace_numel)")
     check(lib().bp_attn_bwd_ex(_dt(qkv), B, S, H, Dh, int(bool(causal)), float(scale), _p(qkv), _p(o), _p(dout),
                                _p(lse), _p(dqkv), _p(workspace), _p(dbias), _s(stream)), "bp_attn_bwd")
 
