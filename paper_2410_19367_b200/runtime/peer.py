@@ -148,7 +148,7 @@ class PeerContext(DistContext):
             name = self._shm.name
         torch.cuda.synchronize(trainer.device)
         hs = lambda pair: [e.ipc_handle() for e in pair]  # noqa: E731
-        info = {"rank": self.rank, "host": socket.gethostname(), "shm": name,
+        info = {"rank": self.rank, "host": socket.gethostname(), "shm": name, "device": trainer.device.index,
                 "slab": _export(self.slab), "slots": dict(self.slot_of),
                 "grads": {(dr.value, s): _export(sp.grad) for (dr, s), sp in trainer.stage_params.items()},
                 "ev_msg": {i: hs(p) for i, p in self.ev_msg.items()},
@@ -172,16 +172,21 @@ class PeerContext(DistContext):
         self.cnt = np.ndarray((n_counters,), dtype=np.int64, buffer=self._shm.buf)
         if self.rank == 0:
             self.cnt[:] = 0
-        dev_t = trainer.device
-        opn = lambda hl: tuple(torch.cuda.Event.from_ipc_handle(dev_t, x) for x in hl)  # noqa: E731
+        # an interprocess event is opened on its EXPORTER's device (as torch's
+        # own CUDA IPC does); a stream may wait on an event of another device
+        def opn(r, hl):
+            dev = torch.device("cuda", infos[r]["device"])
+            return tuple(torch.cuda.Event.from_ipc_handle(dev, x) for x in hl)
+
         self.in_msg = {}
         for k in incoming:
             i = self.key_index[k]
             src = next(r for r in self.senders if i in infos[r]["ev_msg"])
-            self.in_msg[i] = opn(infos[src]["ev_msg"][i])
-        self.p_ready = {s: opn(infos[p]["ev_ready"][s]) for s, p in self.partner.items()}
-        self.p_read = {s: opn(infos[p]["ev_read"][s]) for s, p in self.partner.items()}
-        self.r_free = {r: opn(infos[r]["ev_free"]) for r in self.receivers}
+            self.in_msg[i] = opn(src, infos[src]["ev_msg"][i])
+        self.p_ready = {s: opn(p, infos[p]["ev_ready"][s]) for s, p in self.partner.items()}
+        self.p_read = {s: opn(p, infos[p]["ev_read"][s]) for s, p in self.partner.items()}
+        self.r_free = {r: opn(r, infos[r]["ev_free"]) for r in self.receivers}
+        torch.cuda.set_device(trainer.device)   # (opening may have switched the current device)
         for r in sorted(set(self.receivers) | set(self.partner.values())):
             inf = infos[r]
             rem = {"grads": {}}
