@@ -24,7 +24,7 @@ head and loss.  In the V map both sit on device 0 (down) / D-1 (up).
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import torch
 

@@ -34,7 +34,7 @@ from dataclasses import dataclass
 
 import torch
 
-from ..model import CONFIGS, ModelConfig, OptimConfig, balanced_counts, stage_partition
+from ..model import ModelConfig, OptimConfig, balanced_counts, stage_partition
 from ..schedule import Direction, Schedule, TaskKind, canonical_replay
 from . import ops
 from .compute import StageCompute

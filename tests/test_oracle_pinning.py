@@ -14,7 +14,6 @@ so the oracle is pinned three independent ways:
    (loss AND every parameter gradient);
 3. the single AdamW update against ``torch.optim.AdamW``.
 """
-import math
 
 import pytest
 import torch
