@@ -836,10 +836,15 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
         }
         tmem_st_32x32b_x16(tl + hf * 16, pk);
         tmem_st_32x32b_x16(tl + 64 + hf * 16, dk);
-        if (ds_t) {  // dS^T row of this key, 32 queries (64 B), for the dQ GEMM
-          uint4* dst = reinterpret_cast<uint4*>(ds_t + ((int64_t)bh * S + key) * S + qi * 64 + hf * 32);
+        if (ds_t) {  // dS^T row of this key, 32 queries (64 B), for the dQ GEMM: two
+                     // 256-bit stores, each a whole 32-byte sector (no partial-sector writes)
+          uint32_t* dst = reinterpret_cast<uint32_t*>(ds_t + ((int64_t)bh * S + key) * S + qi * 64 + hf * 32);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) dst[u] = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+          for (int u = 0; u < 2; ++u)
+            asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + 8 * u), "r"(dk[8 * u]),
+                         "r"(dk[8 * u + 1]), "r"(dk[8 * u + 2]), "r"(dk[8 * u + 3]), "r"(dk[8 * u + 4]),
+                         "r"(dk[8 * u + 5]), "r"(dk[8 * u + 6]), "r"(dk[8 * u + 7])
+                         : "memory");
         }
         TRACE(it, 5);
       }
