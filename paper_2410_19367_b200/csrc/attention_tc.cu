@@ -90,6 +90,19 @@ BP_DEV uint4 pack8(const float* f) {
   return u;
 }
 
+// 32 consecutive bf16 (64 B, 32-byte aligned) from 32 floats as two 256-bit
+// stores: whole 32-byte sectors (a thread's row segment; the rows of a warp
+// are strided, so 128-bit stores left every sector half written)
+BP_DEV void st_row32_bf16(__nv_bfloat16* dst, const float* v) {
+  const uint4 a = pack8(v), b = pack8(v + 8), c = pack8(v + 16), d = pack8(v + 24);
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(a.x), "r"(a.y), "r"(a.z),
+               "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + 16), "r"(c.x), "r"(c.y), "r"(c.z),
+               "r"(c.w), "r"(d.x), "r"(d.y), "r"(d.z), "r"(d.w)
+               : "memory");
+}
+
 BP_DEV void st_shared_v4(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
@@ -372,8 +385,7 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       tmem_ld_32x32b_x32(tl + 384 + c * 32, ov);
 #pragma unroll
       for (int i = 0; i < 32; ++i) ov[i] *= inv;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(orow + c * 32 + 8 * u) = pack8(ov + 8 * u);
+      st_row32_bf16(orow + c * 32, ov);
     }
     if (hh == 0) lse[((int64_t)b * H + h) * S + q] = (m_used + log2f(l)) * kLn2;
   }
@@ -611,8 +623,7 @@ fwd2_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__
       tmem_ld_32x32b_x32(tO + c * 32, ov);
 #pragma unroll
       for (int i = 0; i < 32; ++i) ov[i] *= inv;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(orow + c * 32 + 8 * u) = pack8(ov + 8 * u);
+      st_row32_bf16(orow + c * 32, ov);
     }
     lse[((int64_t)b * H + h) * S + q] = (m_used + log2f(l)) * kLn2;
   }
@@ -863,8 +874,7 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
     for (int c = g; c < Dh / 32; c += 2) {
       float v[32];
       tmem_ld_32x32b_x32(te + c * 32, v);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(dvrow + c * 32 + 8 * u) = pack8(v + 8 * u);
+      st_row32_bf16(dvrow + c * 32, v);
       if (dbias) {  // V-bias gradient: column sums of this warp's 32 keys, as stored
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = bf16_round(v[i]);
@@ -873,8 +883,7 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
       tmem_ld_32x32b_x32(te + Dh + c * 32, v);
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] *= scale;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(dkrow + c * 32 + 8 * u) = pack8(v + 8 * u);
+      st_row32_bf16(dkrow + c * 32, v);
       if (dbias) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = bf16_round(v[i]);
@@ -1064,8 +1073,7 @@ dq_tc(const __grid_constant__ CUtensorMap map_q128, const __grid_constant__ CUte
       tmem_ld_32x32b_x32(te + c * 32, v);
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] *= scale;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(dqrow + c * 32 + 8 * u) = pack8(v + 8 * u);
+      st_row32_bf16(dqrow + c * 32, v);
       if (dbias) {  // Q-bias gradient
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = bf16_round(v[i]);
@@ -1178,8 +1186,7 @@ dq_ds_tc(const __grid_constant__ CUtensorMap map_ds, const __grid_constant__ CUt
       tmem_ld_32x32b_x32(te + c * 32, v);
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] *= scale;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(dqrow + c * 32 + 8 * u) = pack8(v + 8 * u);
+      st_row32_bf16(dqrow + c * 32, v);
       if (dbias) {  // Q-bias gradient: column sums of this warp's 32 queries, as stored
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = bf16_round(v[i]);
