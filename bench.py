@@ -59,8 +59,12 @@ def parse():
     ap.add_argument("--replicas", type=int, default=1,
                     help="data-parallel pipeline replicas W (N>1 only): D = world / W, each replica on its own batch")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--partition", default="balanced", choices=["balanced", "uniform"],
-                    help="layer -> stage split: cost-balanced for the schedule (model.balanced_counts) or uniform")
+    ap.add_argument("--dump-task-times", default=None,
+                    help="write the measured per-(direction, stage, kind) task times (ms) and the partition as JSON")
+    ap.add_argument("--partition", default="auto", choices=["auto", "calibrated", "balanced", "uniform"],
+                    help="layer -> stage split (model.resolve_partition): 'calibrated' = measured B200 cost table "
+                         "of the config, replayed as executed (model.calibrated_counts); 'balanced' = FLOP cost "
+                         "model (model.balanced_counts); 'auto' = calibrated when the config has a table")
     return ap.parse_args()
 
 
@@ -144,10 +148,9 @@ def plan(args, D):
 
 def workload_config(cfg, args, approach, policy, sched, G, W):
     """The ``config`` object of the JSON line (identical for both arms)."""
-    from paper_2410_19367_b200.model import balanced_counts, stage_partition
+    from paper_2410_19367_b200.model import load_calibration, resolve_partition
     D, N = sched.D, sched.N
-    counts = (balanced_counts(cfg, sched) if args.partition == "balanced"
-              else [len(p.halfblocks) for p in stage_partition(cfg, sched.num_stages)])
+    counts = resolve_partition(cfg, sched, args.partition)
     M = cfg.micro_batch * cfg.seq
     weights_gb = 2 * cfg.n_params() / 1e9
     act_gb = N * M * cfg.hidden * 2 * 14 * cfg.layers / 1e9 / max(1, G)
@@ -157,7 +160,8 @@ def workload_config(cfg, args, approach, policy, sched, G, W):
             "global_batch": W * N * cfg.micro_batch, "seq_len": cfg.seq, "layers": cfg.layers,
             "hidden": cfg.hidden, "vocab": cfg.vocab,
             "parallelism": f"pp{D} bidirectional" + (f" x dp{W}" if W > 1 else ""),
-            "partition": {"kind": args.partition, "halfblocks_per_stage": counts},
+            "partition": {"kind": ("calibrated" if load_calibration(cfg.name) is not None else "balanced")
+                          if args.partition == "auto" else args.partition, "halfblocks_per_stage": counts},
             "l2": f"inputs larger than L2: {weights_gb:.1f} GB bf16 weights + ~{act_gb:.1f} GB of stashed "
                   f"activations per GPU per step vs 126 MB L2 (no flush needed)"}
 
@@ -245,7 +249,7 @@ def main():
     from paper_2410_19367_b200 import schedule as ps
     from paper_2410_19367_b200.model import CONFIGS, OptimConfig, flops_per_token, synthetic_batch
     from paper_2410_19367_b200.runtime import ops
-    from paper_2410_19367_b200.runtime.executor import Trainer
+    from paper_2410_19367_b200.runtime.executor import Trainer, replay_times
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -348,8 +352,23 @@ def main():
     measured = None
     if world == 1:
         times = tr.measure_task_times()
+        if args.dump_task_times:
+            with open(args.dump_task_times, "w") as f:
+                json.dump({"config": cfg.name, "D": D, "N": N, "partition": [len(p.halfblocks) for p in tr.plans],
+                           "times": [[str(k[0].value), k[1], k[2], v] for k, v in sorted(
+                               times.items(), key=lambda x: (x[0][0].value, x[0][1], x[0][2]))]}, f, indent=0)
         replay = tr.replay_bubble(times)
         replay["tokens_per_s_on_D_gpus"] = tokens_per_step / (replay["makespan_ms"] / 1e3)
+        replay["task_model"] = "paper: every B carries its micro-batch's weight gradients"
+        if tr.deferred_stages:
+            rx = tr.replay_bubble(times, deferred_w=True)
+            rx["tokens_per_s_on_D_gpus"] = tokens_per_step / (rx["makespan_ms"] / 1e3)
+            rx["task_model"] = ("as executed: B = input-gradient chain, each stage replica's deferred "
+                                "weight-gradient GEMMs (K = n_rep M) after its last backward")
+            unit = {k: (1.0 if k[2] == "F" else 2.0 if k[2] == "B" else 1.0 if k[2] == "Bd" else N / len(sched.directions))
+                    for k in times}
+            rx["canonical"] = replay_times(sched, unit, deferred_w=True)["bubble"]
+            replay["as_executed"] = rx
     else:
         # one more step with per-task CUDA events on every rank (relative to a
         # start event recorded right after a barrier), gathered to rank 0:
@@ -448,7 +467,9 @@ def main():
                        "measured": measured,
                        "note": "1 GPU: the D logical devices share the GPU, so pipeline bubbles are filled by other "
                                "streams; measured_replay = ASAP replay of the executed per-device orders with each "
-                               "task's isolated measured device time (one GPU per logical device, free comm)"},
+                               "task's isolated measured device time (one GPU per logical device, free comm); "
+                               "as_executed: the same with the deferred weight gradients as separate drain tasks "
+                               "(canonical = F 1, B 1, W 1 per micro-batch)"},
             "gpu_launches": launches,
             "wgrad": {"deferred_stages": tr.deferred_stages, "combined_stages": sorted(tr.combined_stages),
                       "note": "deferred = one K = N M weight-gradient GEMM per weight at the stage's last "

@@ -29,6 +29,7 @@ from dataclasses import dataclass
 import torch
 
 __all__ = ["ModelConfig", "CONFIGS", "StagePlan", "stage_partition", "balanced_counts", "stage_costs",
+           "fit_task_costs", "modelled_task_times", "calibrated_counts", "load_calibration", "resolve_partition",
            "device_loads", "param_specs", "stage_param_names",
            "init_params", "flops_per_token"]
 
@@ -208,6 +209,139 @@ def balanced_counts(cfg: ModelConfig, schedule) -> list[int]:
                 if sc < best:
                     best, counts, improved = sc, c, True
     return counts
+
+
+# -- measured-cost partitioner ------------------------------------------------
+# Task kinds of the as-executed replay (schedule.analysis.replay_times): F,
+# B (= backward with its micro-batch's weight gradients, the paper's model),
+# Bd (= the input-gradient chain the step runs when weight gradients are
+# deferred) and W (= one stage replica's deferred weight-gradient GEMMs over
+# its n_rep micro-batches).  A stage's time of each kind is modelled as
+# linear in its content: attention half-blocks, MLP half-blocks, the LM head
+# (+ final LN + cross-entropy) and the embedding.
+COST_TERMS = ("attn", "mlp", "head", "embed")
+COST_KINDS = ("F", "B", "Bd", "W")
+
+
+def _stage_terms(counts) -> list:
+    out, start = [], 0
+    S = len(counts)
+    for s, c in enumerate(counts):
+        n_attn = sum(1 for hb in range(start, start + c) if hb % 2 == 0)
+        out.append((n_attn, c - n_attn, 1 if s == S - 1 else 0, 1 if s == 0 else 0))
+        start += c
+    return out
+
+
+def fit_task_costs(counts, times: dict, n_rep: int, *more) -> dict:
+    """Least-squares fit of ``{kind: {term: ms}}`` (COST_KINDS x COST_TERMS)
+    to measured task times ``{(direction, stage, kind): ms}``
+    (``Trainer.measure_task_times``) of a run with partition ``counts``
+    (every direction's replica of a stage is one sample; further runs as
+    ``(counts, times, n_rep)`` triples in ``more``).  W is stored per
+    micro-batch (the measured block covers the replica's ``n_rep``)."""
+    rows, ys = [], {k: [] for k in COST_KINDS}
+    for cnt, tm, nr in ((counts, times, n_rep),) + tuple(more):
+        terms = _stage_terms(cnt)
+        for dr, s, _k in sorted(k for k in tm if k[2] == "F"):
+            rows.append(terms[s])
+            for kind in COST_KINDS:
+                ys[kind].append(tm[(dr, s, kind)] / (nr if kind == "W" else 1))
+    X = torch.tensor(rows, dtype=torch.float64)
+    out = {}
+    for kind in COST_KINDS:
+        y = torch.tensor(ys[kind], dtype=torch.float64)[:, None]
+        c = torch.linalg.lstsq(X, y).solution[:, 0]
+        out[kind] = {t: max(0.0, float(v)) for t, v in zip(COST_TERMS, c)}
+    return out
+
+
+def modelled_task_times(counts, costs: dict, schedule) -> dict:
+    """Task times ``{(direction, stage, kind): ms}`` of partition ``counts``
+    under the linear cost table ``costs`` (``fit_task_costs``; W scaled to
+    the schedule's micro-batches per replica)."""
+    out = {}
+    n_rep = schedule.N // len(schedule.directions)
+    for s, tm in enumerate(_stage_terms(counts)):
+        for kind in COST_KINDS:
+            v = sum(n * costs[kind][t] for n, t in zip(tm, COST_TERMS)) * (n_rep if kind == "W" else 1)
+            for dr in schedule.directions:
+                out[(dr, s, kind)] = v
+    return out
+
+
+def calibrated_counts(cfg: ModelConfig, schedule, costs: dict, *, deferred_w: bool = True, start=None) -> list[int]:
+    """Half-blocks per stage minimising the replayed makespan of
+    ``schedule``'s fixed per-device orders (reference ``list_schedule``,
+    fusion.py:34-77, one GPU per logical device, free communication) under
+    the MEASURED cost table ``costs`` -- as the step executes it
+    (``deferred_w``: weight gradients deferred into one block per stage
+    replica after its last backward; else the paper's B = F + W model).
+    Local search from ``start`` (default :func:`balanced_counts`): move one
+    half-block between any two stages while the makespan (then the most
+    loaded device) improves; every stage but the LM-head stage keeps at least
+    one half-block (no pure pass-through hops).  Deterministic."""
+    from .schedule.analysis import replay_times
+
+    S = schedule.num_stages
+    counts = list(start) if start is not None else balanced_counts(cfg, schedule)
+
+    def score(c):
+        r = replay_times(schedule, modelled_task_times(c, costs, schedule), deferred_w)
+        return (round(r["makespan_ms"], 6), round(max(r["busy_ms_per_device"]), 6))
+
+    best = score(counts)
+    improved = True
+    while improved:
+        improved = False
+        for b in range(S):
+            for j in range(S):
+                if j == b or counts[b] <= (0 if b == S - 1 else 1):
+                    continue
+                c = list(counts)
+                c[b] -= 1
+                c[j] += 1
+                sc = score(c)
+                if sc < best:
+                    best, counts, improved = sc, c, True
+    return counts
+
+
+def load_calibration(name: str):
+    """The committed B200 cost table of config ``name``
+    (``paper_2410_19367_b200/calibration/<name>.json``: ``costs`` as fitted
+    by :func:`fit_task_costs` from a bench run's measured task times, with
+    provenance), or None."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "calibration", f"{name}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f)["costs"]
+
+
+def resolve_partition(cfg: ModelConfig, schedule, partition="balanced") -> list[int]:
+    """Half-blocks per stage for ``partition``: "uniform" (stage_partition's
+    rule), "balanced" (FLOP cost model, :func:`balanced_counts`),
+    "calibrated" (measured B200 cost table of the config,
+    :func:`calibrated_counts`; ValueError when the config has none), "auto"
+    (calibrated when a table exists, else balanced) or explicit counts."""
+    if isinstance(partition, str):
+        if partition == "auto":
+            partition = "calibrated" if load_calibration(cfg.name) is not None else "balanced"
+        if partition == "uniform":
+            return [len(p.halfblocks) for p in stage_partition(cfg, schedule.num_stages)]
+        if partition == "balanced":
+            return balanced_counts(cfg, schedule)
+        if partition == "calibrated":
+            costs = load_calibration(cfg.name)
+            if costs is None:
+                raise ValueError(f"no B200 cost calibration for config {cfg.name!r} "
+                                 f"(tools/calibrate.py writes calibration/<config>.json)")
+            return calibrated_counts(cfg, schedule, costs)
+        raise ValueError(f"unknown partition {partition!r}")
+    return [int(c) for c in partition]
 
 
 def param_specs(cfg: ModelConfig):

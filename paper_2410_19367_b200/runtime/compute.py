@@ -193,11 +193,14 @@ class StageCompute:
         wstream.wait_event(ev)
         fn(wstream)
 
-    def _deferred_wgrads(self, q):
+    def _deferred_wgrads(self, q, rows=None):
         """All of the iteration's weight gradients of this replica (or, with
         shared slots, of both co-resident replicas), one GEMM per weight over
-        the slot_total micro-batch slots (beta = 0)."""
+        the slot_total micro-batch slots (beta = 0).  ``rows`` = (r0, r1)
+        restricts K to those slot rows (one replica's share, for timing)."""
         G, S = self.sp.g, self._slots
+        if rows is not None:
+            S = {k: v[rows[0]:rows[1]] for k, v in S.items()}
         for hb in self.plan.halfblocks:
             l, half = divmod(hb, 2)
             p = f"layers.{l}."

@@ -34,13 +34,15 @@ from dataclasses import dataclass
 
 import torch
 
-from ..model import ModelConfig, OptimConfig, balanced_counts, stage_partition
+from ..model import ModelConfig, OptimConfig, resolve_partition, stage_partition
 from ..schedule import Direction, Schedule, TaskKind, canonical_replay
+from ..schedule.analysis import WeightGradTask, replay_times
 from . import ops
 from .compute import StageCompute
 from .state import GEMM_WEIGHTS, BufferPool, StageParams
 
-__all__ = ["Trainer", "StepOutput", "issue_order", "drive", "choose_deferred_stages"]
+__all__ = ["Trainer", "StepOutput", "issue_order", "drive", "choose_deferred_stages", "replay_times",
+           "WeightGradTask"]
 
 
 @dataclass
@@ -140,14 +142,11 @@ class Trainer:
         self.dirs = list(schedule.directions)
         self.bidir = len(self.dirs) == 2
         self.n_rep = self.N // len(self.dirs)
-        # layer -> stage partition: "uniform", "balanced" (cost-balanced for
-        # this schedule, model.balanced_counts) or explicit half-blocks per stage
-        if partition == "uniform":
-            counts = None
-        elif partition == "balanced":
-            counts = balanced_counts(cfg, schedule)
-        else:
-            counts = list(partition)
+        # layer -> stage partition: "uniform", "balanced" (FLOP-cost-balanced
+        # for this schedule), "calibrated" (measured B200 cost table, replayed
+        # as executed), "auto" or explicit half-blocks per stage
+        # (model.resolve_partition)
+        counts = resolve_partition(cfg, schedule, partition)
         self.plans = stage_partition(cfg, self.S, counts)
         self.partition = [len(p.halfblocks) for p in self.plans]
         self.dist = dist_ctx
@@ -595,10 +594,18 @@ class Trainer:
                 out.setdefault(n, t.detach().float().cpu().clone())
         return out
 
-    def measure_task_times(self, reps: int = 3) -> dict:
+    def measure_task_times(self, reps: int = 7) -> dict:
         """Isolated device time (ms) of every distinct task class of this
-        schedule: {(direction, stage, 'F'|'B'): ms}, each timed alone on one
-        stream with CUDA events (median of ``reps``) on synthetic inputs."""
+        schedule, each timed alone on one stream with CUDA events (median of
+        ``reps``) on synthetic inputs:
+
+        * ``(direction, stage, 'F'|'B')``: forward; backward WITH its
+          per-micro-batch weight-gradient GEMMs (the paper's B = 2F model);
+        * ``(direction, stage, 'Bd')``: backward as the step executes it when
+          the stage defers its weight gradients (input-gradient chain only);
+        * ``(direction, stage, 'W')``: that replica's deferred weight-gradient
+          GEMMs over its n_rep micro-batch slots (K = n_rep M, one GEMM per
+          weight), issued at its last backward; 0 for a non-deferring stage."""
         cfg = self.cfg
         M = cfg.micro_batch * cfg.seq
         dev = self.device
@@ -608,53 +615,79 @@ class Trainer:
         d0 = self.local_devices[0]
         out = {}
         torch.cuda.synchronize(dev)
-        # per-micro-batch weight gradients while timing tasks in isolation
-        # (the deferred one-GEMM-per-weight form only exists at iteration level)
-        deferred = {k: c.defer_wgrad for k, c in self.compute.items()}
-        for c in self.compute.values():
-            c.defer_wgrad = False
-        for (dr, s), comp in self.compute.items():
-            ft, bt = [], []
-            for _ in range(reps + 1):
-                x0 = None if s == 0 else (torch.randn(M, cfg.hidden, device=dev) * 0.1).to(self.dtype)
-                dy = None if s == self.S - 1 else (torch.randn(M, cfg.hidden, device=dev) * 1e-3).to(self.dtype)
-                torch.cuda.synchronize(dev)
-                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-                e0.record(st)
-                stash, msg = comp.forward(st, self.pool, x0=x0, tokens=tok, targets=tok, loss_slot=loss)
-                e1.record(st)
-                dx, release, _ = comp.backward(st, self.pool, stash, dy, self.ws[d0])
-                e2.record(st)
-                torch.cuda.synchronize(dev)
-                ft.append(e0.elapsed_time(e1))
-                bt.append(e1.elapsed_time(e2))
-                ev = torch.cuda.Event()
-                ev.record(st)
-                self.pool.put_all([t for t in release if t is not None] + [msg, dx], ev)
-            out[(dr, s, "F")] = sorted(ft[1:])[len(ft[1:]) // 2]
-            out[(dr, s, "B")] = sorted(bt[1:])[len(bt[1:]) // 2]
+        saved = {k: (c.defer_wgrad, c.combined_wgrad, c._fwd_slot, c._bwd_count) for k, c in self.compute.items()}
+
+        def fb(comp, s):
+            """One forward + backward of ``comp`` on ``st``: (F ms, B ms)."""
+            x0 = None if s == 0 else (torch.randn(M, cfg.hidden, device=dev) * 0.1).to(self.dtype)
+            dy = None if s == self.S - 1 else (torch.randn(M, cfg.hidden, device=dev) * 1e-3).to(self.dtype)
+            torch.cuda.synchronize(dev)
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(st)
+            stash, msg = comp.forward(st, self.pool, x0=x0, tokens=tok, targets=tok, loss_slot=loss)
+            e1.record(st)
+            dx, release, _ = comp.backward(st, self.pool, stash, dy, self.ws[d0])
+            e2.record(st)
+            torch.cuda.synchronize(dev)
+            ev = torch.cuda.Event()
+            ev.record(st)
+            self.pool.put_all([t for t in release if t is not None] + [msg, dx], ev)
+            return e0.elapsed_time(e1), e1.elapsed_time(e2)
+
+        def wblock(comp):
+            """The replica's deferred weight-gradient GEMMs over its own n_rep slots (ms)."""
+            r0 = comp.slot_base * M
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            comp._deferred_wgrads(st, rows=(r0, r0 + comp.n_rep * M))
+            e1.record(st)
+            torch.cuda.synchronize(dev)
+            return e0.elapsed_time(e1)
+
+        # round-robin over the stage replicas, one sample of every task class
+        # per round, so clock drift under the power cap spreads over all
+        # classes instead of biasing the ones measured during a slow spell;
+        # the first round is warm-up, each class reports its median
+        samples: dict = {}
+        for rnd in range(reps + 1):
+            for (dr, s), comp in self.compute.items():
+                deferring = saved[(dr, s)][0]
+                comp.defer_wgrad = False       # per-micro-batch weight gradients (the paper's task model)
+                f, b = fb(comp, s)
+                bd, w = b, 0.0
+                if deferring:
+                    # the executed form: input-gradient chain only (combined_wgrad
+                    # keeps backward() from issuing the deferred GEMMs itself) ...
+                    comp.defer_wgrad, comp.combined_wgrad = True, True
+                    comp._fwd_slot = comp._bwd_count = 0
+                    _, bd = fb(comp, s)
+                    w = wblock(comp)       # ... and this replica's deferred GEMMs
+                    comp.combined_wgrad = saved[(dr, s)][1]
+                if rnd:
+                    for k, v in (("F", f), ("B", b), ("Bd", bd), ("W", w)):
+                        samples.setdefault((dr, s, k), []).append(v)
+        for k, v in samples.items():
+            v.sort()
+            out[k] = v[len(v) // 2]
         for sp in self.stage_params.values():
             sp.grad.zero_()
         for k, c in self.compute.items():
-            c.defer_wgrad = deferred[k]
+            c.defer_wgrad, c.combined_wgrad, c._fwd_slot, c._bwd_count = saved[k]
         return out
 
-    def replay_bubble(self, times: dict) -> dict:
+    def replay_bubble(self, times: dict, deferred_w: bool = False) -> dict:
         """ASAP replay (reference ``list_schedule``, fusion.py:34-77) of the
         executed per-device orders with the MEASURED task times: the makespan
         and bubble the schedule would have with one GPU per logical device and
-        free communication (SPEC.md:263 bubble definition)."""
-        from fractions import Fraction
-        from ..schedule import list_schedule
-        us = {k: Fraction(round(v * 1000)) for k, v in times.items()}   # integer microseconds
-        def dur(t):
-            return us[(t.direction, t.stage, t.kind.value)]
-        starts = list_schedule(self.sched.per_device, self.sched.dependencies, dur)
-        mk = max(st + dur(t) for t, st in starts.items())
-        busy = [sum(dur(t) for t in row) for row in self.sched.per_device]
-        beta = 1 - Fraction(sum(busy)) / (self.D * mk)
-        return {"makespan_ms": float(mk) / 1000, "bubble": float(beta),
-                "busy_ms_per_device": [float(b) / 1000 for b in busy]}
+        free communication (SPEC.md:263 bubble definition).
+
+        ``deferred_w=False``: the paper's task model, every B carrying its
+        micro-batch's weight gradients.  ``deferred_w=True``: the step as it
+        executes -- B is the input-gradient chain ('Bd') and each stage
+        replica's deferred weight-gradient GEMMs ('W') follow its last
+        backward on that device (they fill the pipeline drain); busy time
+        includes them."""
+        return replay_times(self.sched, times, deferred_w)
 
     def timeline_spans(self) -> dict:
         """This process's busy time and first-start / last-end (ms, relative

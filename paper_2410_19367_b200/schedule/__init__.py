@@ -16,7 +16,7 @@ from .builders import (PAPER_GATE_STAGE, build, build_1f1b, build_bitpipe, build
                        merge_bidirectional, paper_policy)
 from .analysis import (CommTotals, analytic_bubble_ratio, analytic_comm_count, analytic_comm_time,
                        analytic_makespan, canonical_bubble, canonical_replay, comm_accounting,
-                       peak_activations, search_bitpipe_policy)
+                       peak_activations, replay_times, search_bitpipe_policy)
 from . import errors
 
 __all__ = [
@@ -30,7 +30,7 @@ __all__ = [
     "schedule_from_dict", "looping_map", "v_shaped_map", "FusedLayout", "LayoutPolicy",
     "fused_layout", "list_schedule", "PAPER_GATE_STAGE", "paper_policy", "peak_activations", "search_bitpipe_policy",
     "analytic_bubble_ratio", "analytic_makespan", "canonical_bubble", "canonical_replay",
-    "CommTotals", "comm_accounting", "analytic_comm_count", "analytic_comm_time",
+    "CommTotals", "comm_accounting", "analytic_comm_count", "analytic_comm_time", "replay_times",
     "errors",
 ]
 

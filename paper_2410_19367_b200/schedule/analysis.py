@@ -14,11 +14,11 @@ from fractions import Fraction
 from .domain import ApproachId, ClusterSpec, ModelProfile, message_size
 from .errors import UnsupportedCombination
 from .layout import list_schedule
-from .plan import Schedule, TaskKind
+from .plan import Direction, Schedule, TaskKind
 
 __all__ = ["analytic_bubble_ratio", "analytic_makespan", "canonical_replay", "canonical_bubble",
            "peak_activations", "search_bitpipe_policy", "CommTotals", "comm_accounting",
-           "analytic_comm_count", "analytic_comm_time"]
+           "analytic_comm_count", "analytic_comm_time", "replay_times", "WeightGradTask"]
 
 
 def analytic_bubble_ratio(approach: ApproachId, D: int, N: int, v: int = 2) -> Fraction:
@@ -89,6 +89,55 @@ def peak_activations(s: Schedule) -> list:
             peak = max(peak, live)
         out.append(Fraction(peak, s.v))
     return out
+
+
+@dataclass(frozen=True)
+class WeightGradTask:
+    """Pseudo-task of the as-executed replay: one stage replica's deferred
+    weight-gradient GEMMs, after its last backward on its device."""
+    stage: int
+    direction: Direction
+
+    @property
+    def key(self) -> tuple:
+        return ("W", self.stage, self.direction)
+
+
+def replay_times(schedule, times: dict, deferred_w: bool = False) -> dict:
+    """ASAP replay of ``schedule``'s per-device orders with measured task
+    times ``{(direction, stage, 'F'|'B'|'Bd'|'W'): ms}`` (see
+    ``Trainer.measure_task_times`` / ``replay_bubble``).  Integer
+    microseconds, exact arithmetic.  Returns makespan, bubble
+    beta = 1 - sum busy / (D makespan) and per-device busy."""
+    us = {k: Fraction(round(v * 1000)) for k, v in times.items()}   # integer microseconds
+    rows = [list(r) for r in schedule.per_device]
+    last_b = {}
+    if deferred_w:
+        for d, pts in schedule.last_backward_positions().items():
+            for (dr, st), i in sorted(pts.items(), key=lambda x: -x[1]):
+                w = WeightGradTask(st, dr)
+                last_b[w.key] = rows[d][i]
+                rows[d].insert(i + 1, w)
+
+    def dur(t):
+        if isinstance(t, WeightGradTask):
+            return us[(t.direction, t.stage, "W")]
+        k = t.kind.value
+        if deferred_w and k == "B":
+            k = "Bd"
+        return us[(t.direction, t.stage, k)]
+
+    def deps(t):
+        if isinstance(t, WeightGradTask):
+            return (last_b[t.key],)
+        return schedule.dependencies(t)
+
+    starts = list_schedule(rows, deps, dur)
+    mk = max(st + dur(t) for t, st in starts.items())
+    busy = [sum(dur(t) for t in row) for row in rows]
+    beta = 1 - Fraction(sum(busy)) / (schedule.D * mk)
+    return {"makespan_ms": float(mk) / 1000, "bubble": float(beta),
+            "busy_ms_per_device": [float(b) / 1000 for b in busy]}
 
 
 def search_bitpipe_policy(D: int, N: int, v: int = 2, max_peak=None):

@@ -122,3 +122,58 @@ def test_analytic_comm_time_table6():
         assert Fraction(ps.analytic_comm_count(A.BITPIPE, D, N), ps.analytic_comm_count(A.DAPPLE_1F1B, D, N)) == 2
     with pytest.raises(ps.errors.UnsupportedCombination):
         ps.analytic_comm_time(A.GPIPE, 4, 4, prof, cl)
+
+
+def _synthetic_costs():
+    return {"F": {"attn": 0.16, "mlp": 0.17, "head": 0.45, "embed": 0.03},
+            "B": {"attn": 0.27, "mlp": 0.31, "head": 0.67, "embed": 0.03},
+            "Bd": {"attn": 0.20, "mlp": 0.16, "head": 0.27, "embed": 0.02},
+            "W": {"attn": 0.05, "mlp": 0.10, "head": 0.33, "embed": 0.01}}
+
+
+def test_fit_task_costs_recovers_a_linear_table():
+    """The least-squares fit of measured task times (model.fit_task_costs)
+    returns the per-term table that generated them (W per micro-batch)."""
+    from paper_2410_19367_b200.model import fit_task_costs, modelled_task_times
+    sched = ps.build_bitpipe(8, 16, policy=ps.paper_policy(8))
+    counts = [3, 3, 3, 2, 4, 3, 3, 3, 3, 3, 3, 2, 4, 4, 4, 1]
+    costs = _synthetic_costs()
+    fit = fit_task_costs(counts, modelled_task_times(counts, costs, sched), 8)
+    for kind in costs:
+        for term in costs[kind]:
+            assert fit[kind][term] == pytest.approx(costs[kind][term], abs=1e-9)
+
+
+@pytest.mark.parametrize("name,D,N", [("gpt-1.3b", 8, 16), ("bert-large", 4, 8)])
+def test_calibrated_partition_shortens_the_as_executed_replay(name, D, N):
+    """The measured-cost partition (model.calibrated_counts) never lengthens
+    the as-executed replay of its start, keeps every non-head stage
+    non-empty, and is deterministic."""
+    from paper_2410_19367_b200.model import calibrated_counts, modelled_task_times, resolve_partition
+    from paper_2410_19367_b200.schedule.analysis import replay_times
+    cfg = CONFIGS[name]
+    sched = ps.build_bitpipe(D, N, policy=ps.paper_policy(D))
+    costs = _synthetic_costs()
+    start = resolve_partition(cfg, sched, "balanced")
+    c = calibrated_counts(cfg, sched, costs, start=start)
+    assert sum(c) == 2 * cfg.layers and min(c[:-1]) >= 1 and c[-1] >= 0
+    assert c == calibrated_counts(cfg, sched, costs, start=start)
+    mk = lambda cc: replay_times(sched, modelled_task_times(cc, costs, sched), True)["makespan_ms"]  # noqa: E731
+    assert mk(c) <= mk(start)
+
+
+def test_resolve_partition_kinds():
+    from paper_2410_19367_b200.model import load_calibration, resolve_partition
+    cfg = CONFIGS["tiny"]
+    sched = ps.build_bitpipe(4, 8)
+    assert resolve_partition(cfg, sched, "uniform") == [len(p.halfblocks) for p in stage_partition(cfg, 8)]
+    assert resolve_partition(cfg, sched, [2, 0, 1, 1, 1, 1, 2, 0]) == [2, 0, 1, 1, 1, 1, 2, 0]
+    assert load_calibration("tiny") is None
+    assert resolve_partition(cfg, sched, "auto") == resolve_partition(cfg, sched, "balanced")
+    with pytest.raises(ValueError, match="calibration"):
+        resolve_partition(cfg, sched, "calibrated")
+    # the committed B200 tables load and give valid partitions
+    for name, D, N in (("gpt-1.3b", 8, 16), ("bert-large", 4, 8)):
+        assert load_calibration(name) is not None
+        c = resolve_partition(CONFIGS[name], ps.build_bitpipe(D, N, policy=ps.paper_policy(D)), "auto")
+        assert sum(c) == 2 * CONFIGS[name].layers

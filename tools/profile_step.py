@@ -16,12 +16,13 @@ ap.add_argument("--D", type=int, default=8)
 ap.add_argument("--N", type=int, default=16)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--order", default="paper", choices=["paper", "search"])
+ap.add_argument("--partition", default="auto")
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
-# the bench's configuration: F2 paper-policy order, cost-balanced partition
+# the bench's configuration: F2 paper-policy order, its default partition ("auto")
 sched = ps.build_bitpipe(args.D, args.N, policy=ps.search_bitpipe_policy(args.D, args.N)[0]
                          if args.order == "search" else ps.paper_policy(args.D))
-tr = Trainer(cfg, sched, dtype=torch.bfloat16, optim=OptimConfig(), partition="balanced")
+tr = Trainer(cfg, sched, dtype=torch.bfloat16, optim=OptimConfig(), partition=args.partition)
 tok, tgt = synthetic_batch(cfg, args.N)
 tok, tgt = tok.int().cuda(), tgt.int().cuda()
 for _ in range(args.warmup):
