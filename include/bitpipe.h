@@ -108,6 +108,10 @@ enum bp_option {
                                 dK/dV kernel stores dS^T (bf16, in the
                                 workspace) and dQ = dS K runs as a GEMM over
                                 it; 1 the dQ kernel recomputes S and dP     */
+  BP_OPT_GEMM_EPI_WARPS = 16, /* 2-SM GEMM epilogue warps: 0 (default) 8 on
+                                launches with one tile per CTA pair (the
+                                epilogue is exposed there), else 4; 4 / 8
+                                force (TMA-store epilogues, no stream-K)    */
 };
 BP_API int bp_set_option(int option, int value);
 

@@ -320,17 +320,18 @@ BP_DEV void epi_tma_prefetch_input(const CUtensorMap* mx, EpiTma& es, int u, int
 template <int NCHUNK, int U = 2>
 BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap* mx, uint32_t tmem_addr,
                          int row0, int lane, int n0, EpiTma& es, bool input_issued, bool etr = false,
-                         const float* sbias = nullptr) {
+                         const float* sbias = nullptr, int nlim = 0x7fffffff) {
+  if (nlim > ep.N) nlim = ep.N;  // columns past the tile (split epilogue) or the matrix are not this warp's
   const bool gelu = ep.epilogue == BP_EPI_GELU;
   const bool has_in = ep.residual != nullptr || ep.epilogue == BP_EPI_DGELU;
   if (has_in && !input_issued && lane == 0) epi_tma_prefetch_input(mx, es, es.ubuf, n0, row0);
 #pragma unroll 1
   for (int c = 0; c < NCHUNK; ++c) {
     const int c0 = n0 + c * 32;
-    if (c0 >= ep.N) break;  // warp-uniform
+    if (c0 >= nlim) break;  // warp-uniform
     const int u = es.ubuf;
     uint8_t* unit = es.stage + u * 4096;
-    if (has_in && lane == 0 && c + 1 < NCHUNK && c0 + 32 < ep.N)
+    if (has_in && lane == 0 && c + 1 < NCHUNK && c0 + 32 < nlim)
       epi_tma_prefetch_input(mx, es, (u + 1) % U, c0 + 32, row0);
     ETRACE(c, 0);
     float v[32];
@@ -617,7 +618,8 @@ BP_DEV unsigned flag_acquire(const unsigned* f) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
   return v;
 }
-BP_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+template <int EW = 4>
+BP_DEV void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory"); }
 
 // ============================================ tcgen05 2-SM (CTA pair) ====
 // Pair tile 256 x 256: each CTA of the cluster holds 128 rows of A and 128
@@ -632,7 +634,11 @@ BP_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 // M = 2048 per-micro-batch shapes) then has its pipeline fill and epilogue
 // overlapped by the other pair's MMAs instead of leaving the tensor pipe
 // idle; no stream-K paths (its owner CTAs spin).
-template <int BN_, bool B_MN_, int OCC_ = 1>
+// EW = epilogue warps: 4 (one per TMEM lane quarter, each drains its 32
+// rows x all BN columns) or 8 (two per lane quarter, each drains half the
+// columns: half the serial chunk chain of a tile's epilogue, which is
+// exposed when a launch has one tile per CTA pair).
+template <int BN_, bool B_MN_, int OCC_ = 1, int EW_ = 4>
 struct Tc2Cfg {
   // BN = pair-tile width; wider than 256 is issued as NSUB MMAs of N = 256
   // per k-step into adjacent TMEM columns (one accumulator buffer then).
@@ -645,12 +651,15 @@ struct Tc2Cfg {
   static constexpr uint32_t SUB_BYTES = B_MN_ ? BCH * 64 * BK * 2 : SUBH * BK * 2;
   static constexpr uint32_t B_BYTES = NSUB * SUB_BYTES;
   static constexpr int OCC = OCC_;
+  static constexpr int EW = EW_;
+  static constexpr int THREADS = 128 + 32 * EW;
+  static_assert(EW == 4 || (EW == 8 && OCC == 1), "8 epilogue warps: the one-pair-per-SM-pair variant");
   // TMA-store staging units per epilogue warp (up to EPI_UNITS - 1 earlier
   // chunks' stores in flight).  Measured with 4: single-tile epilogues no
   // faster (proj fprop 27.7 us either way) and the stage lost to the extra
   // 32 KB slows the long-K launches (fc2 fprop 58.4 -> 60.4 us)
   static constexpr int EPI_UNITS = 2;
-  static constexpr uint32_t EPI_BYTES = 4 * EPI_UNITS * 4096;
+  static constexpr uint32_t EPI_BYTES = EW * EPI_UNITS * 4096;
   static constexpr uint32_t BIAS_BYTES = 4 * BN_;       // the tile's bias columns (fp32)
   static_assert(OCC == 1 || (OCC == 2 && BN_ <= 256), "co-resident variant: one <= 256-column accumulator");
   // per-CTA budget: the SM's 232448 B (OCC = 1), or half of it less the
@@ -662,15 +671,15 @@ struct Tc2Cfg {
   static constexpr int ACC = (OCC == 1 && 2 * BN_ <= 512) ? 2 : 1;  // TMEM accumulator buffers
   static constexpr uint32_t TMEM_COLS = ACC * BN_ <= 256 ? 256 : 512;  // power of two
   static constexpr size_t SMEM = 1024 + STAGES * (size_t)STAGE_BYTES + EPI_BYTES + BIAS_BYTES + 512;  // 512 B barriers
-  static_assert((2 * STAGES + 4 + 4 * EPI_UNITS) * 8 + 4 <= 512, "barrier region");
+  static_assert((2 * STAGES + 4 + EW * EPI_UNITS) * 8 + 4 <= 512, "barrier region");
 };
 
-template <int BN, bool A_MN, bool B_MN, int OCC>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, OCC)
+template <int BN, bool A_MN, bool B_MN, int OCC, int EW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EW, OCC)
 gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_aux,
                 int M, int N, int K, Epi ep, SkWs ws) {
-  using C = Tc2Cfg<BN, B_MN, OCC>;
+  using C = Tc2Cfg<BN, B_MN, OCC, EW>;
   constexpr int BK = C::BK, STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -682,8 +691,8 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* ebar = tempty + 2;  // 4 epilogue warps x EPI_UNITS input-tile barriers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 4 * C::EPI_UNITS);
+  uint64_t* ebar = tempty + 2;  // EW epilogue warps x EPI_UNITS input-tile barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + EW * C::EPI_UNITS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -716,9 +725,9 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     }
     for (int a = 0; a < C::ACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 256);
+      mbar_init(&tempty[a], 2 * 32 * EW);  // every epilogue thread of both CTAs
     }
-    for (int e = 0; e < 4 * C::EPI_UNITS; ++e) mbar_init(&ebar[e], 1);
+    for (int e = 0; e < EW * C::EPI_UNITS; ++e) mbar_init(&ebar[e], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_2sm<C::TMEM_COLS>(tmem_slot);
@@ -808,6 +817,9 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     }
   } else if (warp >= 4) {  // ---------------------- epilogue (both CTAs)
     const int ew = warp - 4;
+    const int q = ew & 3;  // TMEM lane quarter (warp % 4) = rows q*32 .. q*32+31
+    constexpr int HCH = EW == 8 ? (C::BN / 32 + 1) / 2 : C::BN / 32;  // 32-column chunks per warp
+    const int cofs = EW == 8 ? (ew >> 2) * HCH * 32 : 0;             // this warp's first column in the tile
     int it = 0;
     EpiTma es{sEpi + ew * C::EPI_UNITS * 4096, ebar + C::EPI_UNITS * ew, 0, 0u};
     const bool tma_in = ep.tma_store && (ep.residual != nullptr || ep.epilogue == BP_EPI_DGELU);
@@ -823,24 +835,26 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       const int m0 = (tile % tiles_m) * 256 + rank * 128;
       const int n0 = (tile / tiles_m) * C::BN;
       // the first input tile is requested before waiting for the accumulator
-      if (tma_in && sg.role == 0 && lane == 0) epi_tma_prefetch_input(&map_aux, es, es.ubuf, n0, m0 + ew * 32);
+      if (tma_in && sg.role == 0 && lane == 0 && cofs < C::BN && n0 + cofs < N)
+        epi_tma_prefetch_input(&map_aux, es, es.ubuf, n0 + cofs, m0 + q * 32);
       // the tile's bias columns into shared memory, also before the wait: a
       // per-chunk bias load put an L2 round trip on every 32-column chunk
       // (~4 k cycles of a single-tile epilogue, tools/gemm_trace.py)
       const bool sbias = ep.tma_store && ep.bias && sg.role == 0;
       if (sbias) {
-        epi_bar();  // every epilogue warp is done with the previous tile's bias
-        for (int j = ew * 32 + lane; j < C::BN; j += 128)
+        epi_bar<EW>();  // every epilogue warp is done with the previous tile's bias
+        for (int j = ew * 32 + lane; j < C::BN; j += 32 * EW)
           sBias[j] = n0 + j < N ? ld_any(ep.bias, ep.bias_dtype, n0 + j) : 0.f;
-        epi_bar();
+        epi_bar<EW>();
       }
       mbar_wait(&tfull[acc], acc_phase);
       if (si == 0 && ew == 0 && lane == 0) GTRACE(4);
       tc_fence_after();
-      const int row = m0 + ew * 32 + lane;
-      const int lrow = ew * 32 + lane;  // row within this CTA's half tile
-      const uint32_t t0 = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * C::BN;
-      if (OCC == 1 && sg.role == 2) {
+      const int row = m0 + q * 32 + lane;
+      const int lrow = q * 32 + lane;  // row within this CTA's half tile
+      const uint32_t t0 = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::BN;
+      // stream-K roles and the per-thread epilogue: 4 epilogue warps only (launcher)
+      if (EW == 4 && OCC == 1 && sg.role == 2) {
         // contributor: raw fp32 partial -> workspace slot, then publish
         float* dst = ws.part + (((size_t)cid * 2 + rank) * 128 + lrow) * C::BN;
 #pragma unroll 1
@@ -852,9 +866,9 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             reinterpret_cast<float4*>(dst + c * 32)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
         }
         __threadfence();
-        epi_bar();
+        epi_bar<EW>();
         if (ew == 0 && lane == 0) flag_release(&ws.flag[cid * 2 + rank], ws.epoch);
-      } else if (OCC == 1 && sg.role == 1) {
+      } else if (EW == 4 && OCC == 1 && sg.role == 1) {
         // owner: wait for every contributor of this tile, add partials
         const int qlo = sch.contrib_lo(tile);
         for (int q = qlo; q < cid; ++q)
@@ -887,10 +901,10 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           for (int i = 0; i < 32; ++i) v[i] += cur[i];
           if (n0 + c * 32 < N) epi_row32(ep, row, n0 + c * 32, v);
         }
-      } else if (ep.tma_store) {
-        epi_tile_tma<C::BN / 32, C::EPI_UNITS>(ep, &map_c, &map_aux, t0, m0 + ew * 32, lane, n0, es, tma_in,
-                                              si == 0 && ew == 0,
-                                 sbias ? sBias : nullptr);
+      } else if (EW == 8 || ep.tma_store) {
+        if (cofs < C::BN)
+          epi_tile_tma<HCH, C::EPI_UNITS>(ep, &map_c, &map_aux, t0 + cofs, m0 + q * 32, lane, n0 + cofs, es, tma_in,
+                                          si == 0 && ew == 0, sbias ? sBias + cofs : nullptr, n0 + C::BN);
       } else {
         epi_tile<C::BN / 32>(ep, t0, row, n0);
       }
@@ -1097,9 +1111,9 @@ static int sk_workspace(cudaStream_t st, size_t floats, int nflag, SkWs* out) {
 
 int gemm_grid_mode();
 
-template <int BN, bool A_MN, bool B_MN, int OCC>
+template <int BN, bool A_MN, bool B_MN, int OCC, int EW = 4>
 static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
-  using C = Tc2Cfg<BN, B_MN, OCC>;
+  using C = Tc2Cfg<BN, B_MN, OCC, EW>;
   CUtensorMap ma, mb;
   int rc;
   if (!A_MN)
@@ -1126,7 +1140,7 @@ static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
       if ((rc = make_map_dt(&maux, g.residual, g.N, g.M, g.ldr, 32, 32, g.c_dtype, sw))) return rc;
     }
   }
-  auto kern = gemm_tc2_kernel<BN, A_MN, B_MN, OCC>;
+  auto kern = gemm_tc2_kernel<BN, A_MN, B_MN, OCC, EW>;
   static bool attr_set = false;
   if (!attr_set) {
     BP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -1153,22 +1167,26 @@ static int launch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   const bool sk_sub = OCC == 1 && skm != 2 && tiles < pairs && kb >= 64 && tiles * 2 > pairs;
   if (sk_sub) npairs = pairs;
   ws.enable = OCC == 1 && (sk_sub || (skm == 1 && tiles > npairs && tiles % npairs != 0)) ? 1 : 0;
+  if (EW == 8 && (ws.enable || !ep.tma_store)) {
+    set_error("bp_gemm: 8 epilogue warps need the TMA-store epilogue and no stream-K");
+    return BP_ERR_INVALID;
+  }
   if (ws.enable) {
     if (int rc = sk_workspace(st, (size_t)npairs * 2 * 128 * C::BN, npairs * 2, &ws)) return rc;
   }
-  kern<<<2 * npairs, 256, C::SMEM, st>>>(ma, mb, mc, maux, g.M, g.N, g.K, ep, ws);
+  kern<<<2 * npairs, C::THREADS, C::SMEM, st>>>(ma, mb, mc, maux, g.M, g.N, g.K, ep, ws);
   count_launch();
   BP_CHECK_LAUNCH("gemm_tc2");
   return BP_OK;
 }
 
-template <int BN, int OCC = 1>
+template <int BN, int OCC = 1, int EW = 4>
 static int dispatch_tc2_bn(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
-  if (!amn && !bmn) return launch_tc2<BN, false, false, OCC>(g, ep, st);
-  if (!amn && bmn) return launch_tc2<BN, false, true, OCC>(g, ep, st);
-  if (amn && !bmn) return launch_tc2<BN, true, false, OCC>(g, ep, st);
-  return launch_tc2<BN, true, true, OCC>(g, ep, st);
+  if (!amn && !bmn) return launch_tc2<BN, false, false, OCC, EW>(g, ep, st);
+  if (!amn && bmn) return launch_tc2<BN, false, true, OCC, EW>(g, ep, st);
+  if (amn && !bmn) return launch_tc2<BN, true, false, OCC, EW>(g, ep, st);
+  return launch_tc2<BN, true, true, OCC, EW>(g, ep, st);
 }
 
 // Pair-tile width BN in {256, 224, 192, 128}.  Per k-block a CTA streams
@@ -1210,6 +1228,7 @@ int pick_tc2_bn(int M, int N, int pairs, bool b_mn_major) {
 
 int gemm_occ_mode();
 int gemm_grid_mode();
+int gemm_epi_warps_mode();
 
 static int dispatch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   const int pairs = num_sms() / 2;
@@ -1231,6 +1250,22 @@ static int dispatch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
       case 192: return dispatch_tc2_bn<192, 2>(g, ep, st);
       case 128: return dispatch_tc2_bn<128, 2>(g, ep, st);
       default: return dispatch_tc2_bn<256, 2>(g, ep, st);
+    }
+  }
+  // 8 epilogue warps (two per TMEM lane quarter) where a CTA pair has ONE
+  // tile: its epilogue is then not hidden behind a next tile's MMAs, and
+  // halving each warp's chunk chain shortens the exposed part
+  // (BP_OPT_GEMM_EPI_WARPS: 0 auto = single-wave launches, 4 never, 8 always)
+  const int ewm = gemm_epi_warps_mode();
+  const int kb = (g.K + 63) / 64;
+  const bool sk_possible = stream_k_mode() != 2 && tiles < pairs && kb >= 64 && tiles * 2 > pairs;
+  const bool ew8_ok = ep.tma_store && bn <= 256 && !sk_possible && stream_k_mode() != 1;
+  if (ew8_ok && (ewm == 8 || (ewm == 0 && tiles <= pairs))) {
+    switch (bn) {
+      case 224: return dispatch_tc2_bn<224, 1, 8>(g, ep, st);
+      case 192: return dispatch_tc2_bn<192, 1, 8>(g, ep, st);
+      case 128: return dispatch_tc2_bn<128, 1, 8>(g, ep, st);
+      default: return dispatch_tc2_bn<256, 1, 8>(g, ep, st);
     }
   }
   switch (bn) {

@@ -497,3 +497,50 @@ def test_gemm_gpt10b_width(M, N, K, ak, bk):
 def test_attention_gpt10b_width():
     """Causal attention with 32 heads of 128 at s = 2048 (GPT-10B), bf16."""
     _check_attention(torch.bfloat16, 1, 2048, 32, 128, True)
+
+
+@pytest.mark.parametrize("M,N,K,epi", [(2048, 2048, 512, "bias"), (2048, 6144, 256, "bias"), (2048, 2048, 256, "res"),
+                                       (2048, 4096, 256, "gelu"), (1024, 1792, 128, "bias"),
+                                       (300, 416, 128, "res"), (512, 768, 256, "dgelu")])
+def test_gemm_epilogue_warps_bitwise(M, N, K, epi):
+    """4 or 8 epilogue warps (BP_OPT_GEMM_EPI_WARPS; 8 splits each TMEM lane
+    quarter's columns over two warps) and the per-thread store epilogue give
+    bit-identical outputs (C and the GELU pre-activation) for every epilogue
+    kind, one or several tiles per CTA pair, ragged M and N."""
+    from paper_2410_19367_b200.runtime.lib import OPT_GEMM_EPI_WARPS, OPT_GEMM_TMA_STORE
+    dev = "cuda"
+    torch.manual_seed(M + N + K)
+    X = torch.randn(M, K, device=dev).bfloat16()
+    W = (torch.randn(N, K, device=dev) * 0.05).bfloat16()
+    kw = {}
+    if epi in ("bias", "res", "gelu"):
+        kw["bias"] = torch.randn(N, device=dev).bfloat16()
+    if epi == "res":
+        kw["residual"] = torch.randn(M, N, device=dev).bfloat16()
+    if epi == "gelu":
+        kw["epilogue"] = EPI_GELU
+    if epi == "dgelu":
+        kw["aux"] = torch.randn(M, N, device=dev).bfloat16()
+        kw["epilogue"] = EPI_DGELU
+    outs = {}
+    try:
+        for name, tma, ew in (("thread", 0, 0), ("tma4", 1, 4), ("tma8", 1, 8)):
+            ops.set_option(OPT_GEMM_TMA_STORE, tma)
+            ops.set_option(OPT_GEMM_EPI_WARPS, ew)
+            C = torch.full((M, N), 7.0, device=dev, dtype=torch.bfloat16)
+            if epi == "gelu":
+                kw["aux"] = torch.full((M, N), 7.0, device=dev, dtype=torch.bfloat16)
+            ops.gemm(X, W, C, **kw)
+            torch.cuda.synchronize()
+            outs[name] = (C, kw["aux"].clone() if epi == "gelu" else None)
+    finally:
+        ops.set_option(OPT_GEMM_TMA_STORE, 1)
+        ops.set_option(OPT_GEMM_EPI_WARPS, 0)
+    ref = outs["thread"]
+    for name in ("tma4", "tma8"):
+        for i in range(2):
+            if ref[i] is None:
+                continue
+            assert torch.isfinite(ref[i].float()).all()
+            bad = (outs[name][i].view(torch.int16) != ref[i].view(torch.int16)).nonzero()
+            assert bad.numel() == 0, (name, i, int(bad.shape[0]), bad[:4].tolist())
