@@ -296,7 +296,11 @@ def main():
     for _ in range(args.warmup):
         tr.train_step(tok_d, tgt_d)
     barrier()
-    graphed = world == 1 and os.environ.get("BP_GRAPH", "0") == "1"
+    # co-resident (1 process): the step is captured once as a CUDA graph and
+    # replayed (BP_GRAPH=0: eager launches).  Measured: BERT-large D=4 N=8
+    # +1.5-2.5 % (the host enqueues ~13 us per launch, ~43 ms per 58 ms
+    # step), GPT-1.3B +0.4 %
+    graphed = world == 1 and os.environ.get("BP_GRAPH", "1") == "1"
     if graphed:  # capture one iteration as a CUDA graph (one more warm-up step), replay it in the timed region
         l0 = ops.launch_count()
         tr.train_step(tok_d, tgt_d)
@@ -406,6 +410,7 @@ def main():
     Mtok = cfg.micro_batch * cfg.seq
     # (distributed: each rank's compute and weight-gradient streams serialised
     # likewise; its per-stage optimizer streams only run AdamW)
+    tr.disable_graph()  # the probe times each launch through the host wrappers
     tr.streams = {d: main_stream for d in tr.streams}
     tr.wstreams = {}  # weight-gradient GEMMs serialised too (their spans would include cross-stream waits)
     if world == 1:
@@ -477,6 +482,7 @@ def main():
             "transport": (dist_ctx.transport if dist_ctx is not None else "co-resident (stream events)")
                          + (" -- ALL RANKS SHARE ONE GPU (BP_SHARE_GPU=1): functional test, not a multi-GPU number"
                             if shared else ""),
+            "launch": "CUDA graph replay of the captured step" if graphed else "eager launches",
             "clocks": clocks,
         }
         if rank == 0 and os.environ.get("BP_SKIP_CPU_BASELINE") != "1":

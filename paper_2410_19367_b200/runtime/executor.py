@@ -373,6 +373,16 @@ class Trainer:
             raise RuntimeError("disable record_timeline to capture the step")
         self._graph_state = "capture"
 
+    def disable_graph(self) -> None:
+        """Back to eager launches from the next ``train_step`` on (the
+        captured graph is dropped; its buffers stay the pool's)."""
+        if self._graph_state is None:
+            return
+        torch.cuda.synchronize(self.device)
+        self._graph, self._graph_state = None, None
+        self.iter_done = None
+        self.pool.forget_events()
+
     def _graph_step(self, tokens, targets) -> StepOutput:
         if self._graph_state == "capture":
             self._g_tok = tokens.clone()
