@@ -112,6 +112,9 @@ enum bp_option {
                                 launches with one tile per CTA pair (the
                                 epilogue is exposed there), else 4; 4 / 8
                                 force (TMA-store epilogues, no stream-K)    */
+  BP_OPT_ATTN_FWD_EXF = 17,   /* tcgen05 attention fwd (one query tile per
+                                CTA): exponentials per 8 computed on the FMA
+                                pipe instead of the MUFU, 2..5 (0: default) */
 };
 BP_API int bp_set_option(int option, int value);
 

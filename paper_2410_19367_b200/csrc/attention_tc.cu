@@ -29,6 +29,7 @@ void count_launch();
 int num_sms();
 bool opt_attn_no_tc();
 int attn_fwd_mode();
+int attn_fwd_exf();
 int attn_bwd_mode();
 int64_t attn_ds_offset_floats(int B, int S, int H);
 int make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, int64_t ld, uint32_t box_inner,
@@ -76,6 +77,50 @@ BP_DEV float ex2_fma(float x) {
   p = fmaf(f, p, 0.99992828f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
+// Packed fp32 pairs (sm_100: FFMA2 / FADD2 -- one issue slot for two
+// lanes' worth of work) and the 3-input max (FMNMX3): the forward softmax is
+// issue-bound (tools/attn_fwd_trace.py), so these cut its instruction count
+// without changing a single rounding (same .rn ops per element).
+BP_DEV uint64_t f2pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+BP_DEV void f2unpack(uint64_t v, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
+BP_DEV uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+BP_DEV uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+BP_DEV float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// ex2_fma on a packed pair (same split and cubic, FFMA2 / FADD2)
+BP_DEV uint64_t ex2_fma2(float x0, float x1) {
+  const uint64_t x = f2pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+  const uint64_t mg = f2pack(12582912.f, 12582912.f), nmg = f2pack(-12582912.f, -12582912.f);
+  const uint64_t t = fadd2(x, mg);
+  float t0, t1, u0, u1;
+  f2unpack(fadd2(t, nmg), u0, u1);
+  const uint64_t f = fadd2(x, f2pack(-u0, -u1));
+  uint64_t p = ffma2(f, f2pack(0.05517025f, 0.05517025f), f2pack(0.24260790f, 0.24260790f));
+  p = ffma2(f, p, f2pack(0.69326093f, 0.69326093f));
+  p = ffma2(f, p, f2pack(0.99992828f, 0.99992828f));
+  float p0, p1;
+  f2unpack(p, p0, p1);
+  f2unpack(t, t0, t1);
+  return f2pack(__int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23)),
+                __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
+}
+
 BP_DEV float lds(uint32_t addr) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
@@ -143,7 +188,31 @@ struct Fwd {
   static constexpr size_t SMEM = 1024 + TILE + KS * TILE + 2 * TILE + 2048 + 512;
 };
 
-template <int Dh, bool CAUSAL>
+// EXF of every 8 exponentials run on the FMA pipe (ex2_fma), the rest on
+// the MUFU (16 lanes / clk / SM: the softmax's exponential phase is
+// MUFU-bound at EXF = 2, tools/attn_fwd_trace.py)
+template <int EXF>
+BP_DEV bool exp_on_fma(int i) {
+  const int k = i & 7;
+  if (EXF <= 0 || EXF >= 6) return false;
+  if (EXF == 2) return k == 3 || k == 7;
+  if (EXF == 3) return k == 2 || k == 5 || k == 7;
+  if (EXF == 4) return (k & 1) == 1;
+  if (EXF == 5) return (k & 1) == 1 || k == 4;
+  return k == 3 || k == 7;
+}
+// EXF >= 6: whole pairs on the FMA pipe (packed ex2_fma2): EXF - 4 of the 8
+// pairs of every 16 exponentials
+template <int EXF>
+BP_DEV bool pair_on_fma(int i) {
+  const int k = (i >> 1) & 7;
+  if (EXF == 6) return k == 3 || k == 7;
+  if (EXF == 7) return k == 2 || k == 5 || k == 7;
+  if (EXF == 8) return (k & 1) == 1;
+  return false;
+}
+
+template <int Dh, bool CAUSAL, int EXF = 2>
 __global__ void __launch_bounds__(384, 1)
 fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ o, float* __restrict__ lse, int S,
        int H, float scale_log2) {
@@ -251,7 +320,9 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       tc_fence_after();
       auto issue_s = [&](int j) {   // S(j) into buffer j % 3
         const int sb = j % 3, ks_ = j % KS;
+        TRACE_MMA(32 + j, 11);
         mbar_wait(&k_full[ks_], (j / KS) & 1);
+        TRACE_MMA(32 + j, 12);
         mbar_wait(&s_free[sb], ((j / 3) & 1) ^ 1);   // every softmax thread has read S(j - 3)
         TRACE_MMA(32 + j, 8);
         tc_fence_after();
@@ -266,7 +337,9 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       if (n_kv > 1) issue_s(1);
       for (int jj = 0; jj < n_kv; ++jj) {
         const int vs = jj & 1;
+        TRACE_MMA(32 + jj, 13);
         mbar_wait(&p_full[jj & 3], (jj >> 2) & 1);
+        TRACE_MMA(32 + jj, 14);
         mbar_wait(&v_full[vs], (jj >> 1) & 1);
         TRACE_MMA(32 + jj, 9);
         tc_fence_after();
@@ -274,6 +347,7 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
           tc_mma_f16_ts(tmem + 384, tmem + (jj % 3) * 128 + 8 * ks, mndesc(aV, ks, 128), idesc_o, (jj > 0 || ks > 0));
+        TRACE_MMA(32 + jj, 15);
         tc_commit(pv_done);
         tc_commit(&v_empty[vs]);
         if (jj == n_kv - 1) tc_commit(o_done);
@@ -302,21 +376,17 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       TRACE(32 + j, 2);
       const bool diag = CAUSAL && (j == qt);
       // max over the raw scores (scale > 0), the scale folds into the exponent FMA
-      float m8[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) m8[e] = -INFINITY;
       if (diag) {
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
+        for (int i = 0; i < 64; ++i)
           if (hh * 64 + i > r) s[i] = -INFINITY;
-          m8[i & 7] = fmaxf(m8[i & 7], s[i]);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) m8[i & 7] = fmaxf(m8[i & 7], s[i]);
       }
-      float mx = scale_log2 * fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                                    fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      float m4[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) m4[e] = fmaxf(s[2 * e], s[2 * e + 1]);
+#pragma unroll
+      for (int i = 8; i < 64; i += 2) m4[(i >> 1) & 3] = fmax3(m4[(i >> 1) & 3], s[i], s[i + 1]);
+      float mx = scale_log2 * fmax3(fmaxf(m4[0], m4[1]), m4[2], m4[3]);
       float* xs = sX + (j & 1) * 256;
       xs[hh * 128 + r] = mx;
       named_bar_sync(1 + wq, 64);
@@ -344,15 +414,28 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       }
       if (up) m_used = mx;
       TRACE(32 + j, 4);
+      // x = s scale - m and the row-sum partials on packed pairs: l2[k] holds
+      // the partial sums of elements i = 8n + 2k, 8n + 2k + 1
+      const uint64_t sc2 = f2pack(scale_log2, scale_log2), nm2 = f2pack(-m_used, -m_used);
+      uint64_t l2[4];
+#pragma unroll
+      for (int i = 0; i < 64; i += 2) {
+        float x0, x1;
+        f2unpack(ffma2(f2pack(s[i], s[i + 1]), sc2, nm2), x0, x1);
+        uint64_t e2;
+        if (EXF >= 6 && pair_on_fma<EXF>(i)) {
+          e2 = ex2_fma2(x0, x1);
+          f2unpack(e2, s[i], s[i + 1]);
+        } else {
+          s[i] = exp_on_fma<EXF>(i) ? ex2_fma(x0) : ex2(x0);  // EXF / 8 on the FMA pipe
+          s[i + 1] = exp_on_fma<EXF>(i + 1) ? ex2_fma(x1) : ex2(x1);
+          e2 = f2pack(s[i], s[i + 1]);
+        }
+        l2[(i >> 1) & 3] = i < 8 ? e2 : fadd2(l2[(i >> 1) & 3], e2);
+      }
       float l8[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) l8[e] = 0.f;
-#pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        const float x = fmaf(s[i], scale_log2, -m_used);
-        s[i] = (i & 3) == 3 ? ex2_fma(x) : ex2(x);  // a quarter on the FMA pipe
-        l8[i & 7] += s[i];
-      }
+      for (int e = 0; e < 4; ++e) f2unpack(l2[e], l8[2 * e], l8[2 * e + 1]);
       l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
       TRACE(32 + j, 5);
       // P (bf16 pairs) over this half's 32 of the S buffer's first 64 columns
@@ -548,9 +631,10 @@ fwd2_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__
       const bool diag = CAUSAL && j == qt;
       // 8 independent max / sum accumulators: a single running fmaxf / fadd
       // is a 128-long dependency chain (~4 cycles per link)
-      float m8[8];
+      // (3-input maxima: 4 accumulators, two scores per FMNMX3)
+      float m4[4];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) m8[e] = -INFINITY;
+      for (int e = 0; e < 4; ++e) m4[e] = -INFINITY;
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         float s[64];
@@ -558,14 +642,13 @@ fwd2_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__
                                 *reinterpret_cast<float(*)[32]>(s + 32));
         if (diag) {
 #pragma unroll
-          for (int i = 0; i < 64; ++i) m8[i & 7] = fmaxf(m8[i & 7], 64 * hf + i > r ? -INFINITY : s[i]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 64; ++i) m8[i & 7] = fmaxf(m8[i & 7], s[i]);
+          for (int i = 0; i < 64; ++i)
+            if (64 * hf + i > r) s[i] = -INFINITY;
         }
+#pragma unroll
+        for (int i = 0; i < 64; i += 2) m4[(i >> 1) & 3] = fmax3(m4[(i >> 1) & 3], s[i], s[i + 1]);
       }
-      const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                             fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      const float mx = fmax3(fmaxf(m4[0], m4[1]), m4[2], m4[3]);
       if (threadIdx.x == 96) TRACE_MMA(32 + j, 2);
       const float mxs = mx * scale_log2;
       const bool up = mxs > m_used + 8.f;  // warp-uniform rescale (see fwd_tc)
@@ -583,29 +666,34 @@ fwd2_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__
       }
       if (up) m_used = mxs;
       if (threadIdx.x == 96) TRACE_MMA(32 + j, 3);
-      float l8[8];
+      // x = s scale - m and the row-sum partials on packed pairs (FFMA2 /
+      // FADD2; l2[k] = the partial sums of elements 8n + 2k, 8n + 2k + 1)
+      const uint64_t sc2 = f2pack(scale_log2, scale_log2), nm2 = f2pack(-m_used, -m_used);
+      uint64_t l2[4];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) l8[e] = 0.f;
+      for (int e = 0; e < 4; ++e) l2[e] = 0;  // +0.0f pairs
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         float s[64];
         tmem_ld_32x32b_x32_pair(tS + 64 * hf, tS + 64 * hf + 32, *reinterpret_cast<float(*)[32]>(s),
                                 *reinterpret_cast<float(*)[32]>(s + 32));
-        if (diag) {
 #pragma unroll
-          for (int i = 0; i < 64; ++i) s[i] = 64 * hf + i > r ? 0.f : ex2(fmaf(s[i], scale_log2, -m_used));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 64; ++i) s[i] = ex2(fmaf(s[i], scale_log2, -m_used));
+        for (int i = 0; i < 64; i += 2) {
+          float x0, x1;
+          f2unpack(ffma2(f2pack(s[i], s[i + 1]), sc2, nm2), x0, x1);
+          s[i] = diag && 64 * hf + i > r ? 0.f : ex2(x0);
+          s[i + 1] = diag && 64 * hf + i + 1 > r ? 0.f : ex2(x1);
+          l2[(i >> 1) & 3] = fadd2(l2[(i >> 1) & 3], f2pack(s[i], s[i + 1]));
         }
-#pragma unroll
-        for (int i = 0; i < 64; ++i) l8[i & 7] += s[i];
         float pk[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) pk[i] = __uint_as_float(pack_bf16x2(s[2 * i], s[2 * i + 1]));
         // P columns [32 hf, 32 hf + 32) overwrite S columns already read
         tmem_st_32x32b_x32(tS + 32 * hf, pk);
       }
+      float l8[8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) f2unpack(l2[e], l8[2 * e], l8[2 * e + 1]);
       l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
       if (threadIdx.x == 96) TRACE_MMA(32 + j, 4);
       tc_fence_before();
@@ -1256,11 +1344,15 @@ static int fwd(int B, int S, int H, float scale, const void* qkv, void* o, float
     BP_CHECK_LAUNCH("attn_fwd2_tc");
     return BP_OK;
   }
-  auto k = fwd_tc<Dh, CAUSAL>;
-  static bool once = false;
-  if (!once) {
+  const int exf = attn_fwd_exf();  // BP_OPT_ATTN_FWD_EXF (0: default)
+  auto k = exf == 3 ? fwd_tc<Dh, CAUSAL, 3> : exf == 4 ? fwd_tc<Dh, CAUSAL, 4> : exf == 5 ? fwd_tc<Dh, CAUSAL, 5>
+          : exf == 6 ? fwd_tc<Dh, CAUSAL, 6> : exf == 7 ? fwd_tc<Dh, CAUSAL, 7> : exf == 8 ? fwd_tc<Dh, CAUSAL, 8>
+                                                                             : fwd_tc<Dh, CAUSAL, 2>;
+  static bool once[7] = {false, false, false, false, false, false, false};
+  const int oi = exf >= 3 && exf <= 8 ? exf - 2 : 0;
+  if (!once[oi]) {
     if (int rc = set_smem(k, Fwd<Dh>::SMEM)) return rc;
-    once = true;
+    once[oi] = true;
   }
   k<<<dim3(B * H, S / 128), 384, Fwd<Dh>::SMEM, st>>>(m, (__nv_bfloat16*)o, lse, S, H, scale * kLog2e);
   count_launch();

@@ -34,7 +34,7 @@ buf = (ctypes.c_longlong * 1024)()
 fn(buf, 1024)
 t = [[buf[i * 16 + k] for k in range(16)] for i in range(64)]
 names = ["wait_S", "tmem_ld", "max+xchg", "rescale", "exp", "pack", "st+arr", "->next"]
-print("j    " + " ".join(f"{n:>8s}" for n in names) + " | rel: S_iss PV_iss K_iss")
+print("j    " + " ".join(f"{n:>8s}" for n in names) + " | rel: S_iss PV_iss K_iss S_top S_kok PV_top PV_pok PV_mmas")
 tot = 0
 for j in range(16):
     row = t[32 + j]
@@ -42,7 +42,7 @@ for j in range(16):
         break
     nxt = t[33 + j][0] if j < 15 else 0
     d = [row[k + 1] - row[k] for k in range(7)] + [(nxt - row[7]) if nxt else 0]
-    rel = [row[k] - row[0] if row[k] else 0 for k in (8, 9, 10)]
+    rel = [row[k] - row[0] if row[k] else 0 for k in (8, 9, 10, 11, 12, 13, 14, 15)]
     if nxt:
         tot += nxt - row[0]
     print(f"{j:4d} " + " ".join(f"{x:8d}" for x in d) + " | " + " ".join(f"{x:7d}" for x in rel))
