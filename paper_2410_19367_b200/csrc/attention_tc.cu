@@ -97,6 +97,23 @@ BP_DEV uint64_t fadd2(uint64_t a, uint64_t b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+BP_DEV uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// P^T = 2^(s scale - lse log2 e) and dS^T = P^T (dP^T - delta) for a pair of
+// queries (FMUL2 / FFMA2 / FADD2 / FMUL2: the roundings of the scalar form)
+BP_DEV void pds2(float& s0, float& s1, float& d0, float& d1, float l0, float l1, float dl0, float dl1,
+                 uint64_t sc2) {
+  const uint64_t nl = fmul2(f2pack(l0, l1), f2pack(-kLog2e, -kLog2e));
+  float x0, x1;
+  f2unpack(ffma2(f2pack(s0, s1), sc2, nl), x0, x1);
+  s0 = ex2(x0);
+  s1 = ex2(x1);
+  f2unpack(fmul2(f2pack(s0, s1), fadd2(f2pack(d0, d1), f2pack(-dl0, -dl1))), d0, d1);
+}
+
 BP_DEV float fmax3(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
@@ -910,17 +927,13 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
             }
           }
         } else {
+          const uint64_t sc2 = f2pack(scale_log2, scale_log2);
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const float4 l4 = lds4(aL + 4 * (hf * 32 + 4 * k)), d4 = lds4(aL + 256 + 4 * (hf * 32 + 4 * k));
-            const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dl[4] = {d4.x, d4.y, d4.z, d4.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int i = 4 * k + e;
-              const float p = ex2(fmaf(sv[i], scale_log2, -lv[e] * kLog2e));
-              sv[i] = p;
-              dp[i] = p * (dp[i] - dl[e]);
-            }
+            const int i = 4 * k;
+            pds2(sv[i], sv[i + 1], dp[i], dp[i + 1], l4.x, l4.y, d4.x, d4.y, sc2);
+            pds2(sv[i + 2], sv[i + 3], dp[i + 2], dp[i + 3], l4.z, l4.w, d4.z, d4.w, sc2);
           }
         }
         TRACE(it, 4);
