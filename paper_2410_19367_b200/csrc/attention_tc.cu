@@ -893,6 +893,7 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
     const int r = wq * 32 + lane;  // key row in the tile
     const int key = kt * 128 + r;
     const uint32_t tl = tmem + ((uint32_t)(wq * 32) << 16) + g * 128;
+    const uint64_t ds_pol = l2_policy_evict_last();
     for (int it = g; it < n_it; it += 2) {
       const int st = it % QST, qi = q0 + it, u = it >> 1;
       TRACE(it, 0);
@@ -949,13 +950,15 @@ dkdv_tc(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUte
         tmem_st_32x32b_x16(tl + hf * 16, pk);
         tmem_st_32x32b_x16(tl + 64 + hf * 16, dk);
         if (ds_t) {  // dS^T row of this key, 32 queries (64 B), for the dQ GEMM: two
-                     // 256-bit stores, each a whole 32-byte sector (no partial-sector writes)
+                     // 256-bit stores, each a whole 32-byte sector (no partial-sector writes),
+                     // evict_last in L2: the dQ GEMM reads them right after this kernel
           uint32_t* dst = reinterpret_cast<uint32_t*>(ds_t + ((int64_t)bh * S + key) * S + qi * 64 + hf * 32);
 #pragma unroll
           for (int u = 0; u < 2; ++u)
-            asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + 8 * u), "r"(dk[8 * u]),
-                         "r"(dk[8 * u + 1]), "r"(dk[8 * u + 2]), "r"(dk[8 * u + 3]), "r"(dk[8 * u + 4]),
-                         "r"(dk[8 * u + 5]), "r"(dk[8 * u + 6]), "r"(dk[8 * u + 7])
+            asm volatile("st.global.L2::cache_hint.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;" ::"l"(dst + 8 * u),
+                         "r"(dk[8 * u]), "r"(dk[8 * u + 1]), "r"(dk[8 * u + 2]), "r"(dk[8 * u + 3]),
+                         "r"(dk[8 * u + 4]), "r"(dk[8 * u + 5]), "r"(dk[8 * u + 6]), "r"(dk[8 * u + 7]),
+                         "l"(ds_pol)
                          : "memory");
         }
         TRACE(it, 5);
@@ -1245,6 +1248,7 @@ dq_ds_tc(const __grid_constant__ CUtensorMap map_ds, const __grid_constant__ CUt
 
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------ producer
+      const uint64_t ds_pol = l2_policy_evict_first();  // the last read of dS^T
       for (int it = 0; it < n_it; ++it) {
         const int st = it % ST;
         mbar_wait(&empty[st], ((it / ST) & 1) ^ 1);
@@ -1252,7 +1256,7 @@ dq_ds_tc(const __grid_constant__ CUtensorMap map_ds, const __grid_constant__ CUt
         // dS^T rows (bh S + keys), query columns in two 64-wide boxes
 #pragma unroll
         for (int c = 0; c < 2; ++c)
-          tma_load_2d(sA0 + st * C::AT + c * 8192, &map_ds, qt * 128 + c * 64, bh * S + kr, &full[st]);
+          tma_load_2d_hint(sA0 + st * C::AT + c * 8192, &map_ds, qt * 128 + c * 64, bh * S + kr, &full[st], ds_pol);
 #pragma unroll
         for (int c = 0; c < C::DC; ++c)
           tma_load_2d(sB0 + st * C::BT + c * 8192, &map_kv64, HD + h * Dh + c * 64, b * S + kr, &full[st]);
