@@ -115,6 +115,11 @@ enum bp_option {
   BP_OPT_ATTN_FWD_EXF = 17,   /* tcgen05 attention fwd (one query tile per
                                 CTA): exponentials per 8 computed on the FMA
                                 pipe instead of the MUFU, 2..5 (0: default) */
+  BP_OPT_GEMM_L2_HINTS = 18,  /* 1 (default): the GELU GEMM's saved pre-
+                                activation is stored L2 evict_first (only
+                                the backward reads it) and read evict_first
+                                by the dGELU epilogue (its last use); 0:
+                                default policy                               */
 };
 BP_API int bp_set_option(int option, int value);
 

@@ -39,6 +39,7 @@ struct Epi {
   int nostore;  // debug: drain TMEM but skip the global epilogue (BP_OPT_GEMM_DEBUG)
   int tma_store;  // 2-SM kernel: stage 32-column chunks in smem, TMA-store them
   float* colsum;  // optional: colsum[n] += sum over rows of C as stored (TMA epilogue only)
+  int aux_evict_first;  // GELU pre-activation (read only by the backward, much later): streamed past L2
 };
 
 BP_DEV float ld_any(const void* p, int dtype, int64_t i) {
@@ -308,11 +309,15 @@ struct EpiTma {
 // The extra epilogue input (residual, or the saved pre-activation for
 // dGELU) arrives by TMA too: chunk c+1's 32 x 32 tile is requested while
 // chunk c is finished, into the upper half of the other unit.
-BP_DEV void epi_tma_prefetch_input(const CUtensorMap* mx, EpiTma& es, int u, int c0, int row0) {
+BP_DEV void epi_tma_prefetch_input(const CUtensorMap* mx, EpiTma& es, int u, int c0, int row0,
+                                   bool last_use = false) {
   uint8_t* dst = es.stage + u * 4096 + 2048;
   fence_proxy_async_smem();  // earlier generic reads of this half precede the async write
   mbar_expect_tx(&es.bar[u], 2048);
-  tma_load_2d(dst, mx, c0, row0, &es.bar[u]);
+  if (last_use)  // the dGELU pre-activation: its last read, leave L2 first
+    tma_load_2d_hint(dst, mx, c0, row0, &es.bar[u], l2_policy_evict_first());
+  else
+    tma_load_2d(dst, mx, c0, row0, &es.bar[u]);
 }
 
 // U staging units per epilogue warp: up to U - 1 TMA stores of earlier
@@ -324,7 +329,7 @@ BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap
   if (nlim > ep.N) nlim = ep.N;  // columns past the tile (split epilogue) or the matrix are not this warp's
   const bool gelu = ep.epilogue == BP_EPI_GELU;
   const bool has_in = ep.residual != nullptr || ep.epilogue == BP_EPI_DGELU;
-  if (has_in && !input_issued && lane == 0) epi_tma_prefetch_input(mx, es, es.ubuf, n0, row0);
+  if (has_in && !input_issued && lane == 0) epi_tma_prefetch_input(mx, es, es.ubuf, n0, row0, ep.aux_evict_first && ep.epilogue == BP_EPI_DGELU);
 #pragma unroll 1
   for (int c = 0; c < NCHUNK; ++c) {
     const int c0 = n0 + c * 32;
@@ -332,7 +337,7 @@ BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap
     const int u = es.ubuf;
     uint8_t* unit = es.stage + u * 4096;
     if (has_in && lane == 0 && c + 1 < NCHUNK && c0 + 32 < nlim)
-      epi_tma_prefetch_input(mx, es, (u + 1) % U, c0 + 32, row0);
+      epi_tma_prefetch_input(mx, es, (u + 1) % U, c0 + 32, row0, ep.aux_evict_first && ep.epilogue == BP_EPI_DGELU);
     ETRACE(c, 0);
     float v[32];
     tmem_ld_32x32b_x32(tmem_addr + c * 32, v);
@@ -394,7 +399,12 @@ BP_DEV void epi_tile_tma(const Epi& ep, const CUtensorMap* mc, const CUtensorMap
         tma_reduce_add_2d(mc, unit, c0, row0);
       else
         tma_store_2d(mc, unit, c0, row0);
-      if (gelu) tma_store_2d(mx, unit + 2048, c0, row0);
+      if (gelu) {
+        if (ep.aux_evict_first)
+          tma_store_2d_hint(mx, unit + 2048, c0, row0, l2_policy_evict_first());
+        else
+          tma_store_2d(mx, unit + 2048, c0, row0);
+      }
       bulk_commit();
     }
     ETRACE(c, 4);
@@ -836,7 +846,8 @@ gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       const int n0 = (tile / tiles_m) * C::BN;
       // the first input tile is requested before waiting for the accumulator
       if (tma_in && sg.role == 0 && lane == 0 && cofs < C::BN && n0 + cofs < N)
-        epi_tma_prefetch_input(&map_aux, es, es.ubuf, n0 + cofs, m0 + q * 32);
+        epi_tma_prefetch_input(&map_aux, es, es.ubuf, n0 + cofs, m0 + q * 32,
+                               ep.aux_evict_first && ep.epilogue == BP_EPI_DGELU);
       // the tile's bias columns into shared memory, also before the wait: a
       // per-chunk bias load put an L2 round trip on every 32-column chunk
       // (~4 k cycles of a single-tile epilogue, tools/gemm_trace.py)
@@ -1229,6 +1240,7 @@ int pick_tc2_bn(int M, int N, int pairs, bool b_mn_major) {
 int gemm_occ_mode();
 int gemm_grid_mode();
 int gemm_epi_warps_mode();
+int gemm_l2_hints();
 
 static int dispatch_tc2(const bp_gemm_args& g, const Epi& ep, cudaStream_t st) {
   const int pairs = num_sms() / 2;
@@ -1318,6 +1330,7 @@ extern "C" int bp_gemm(const bp_gemm_args* gp, void* stream) {
   ep.M = g.M; ep.N = g.N; ep.C = g.C; ep.ldc = g.ldc; ep.c_dtype = g.c_dtype; ep.alpha = g.alpha;
   ep.accumulate = g.beta != 0.f; ep.bias = g.bias; ep.bias_dtype = g.in_dtype;
   ep.residual = g.residual; ep.ldr = g.ldr; ep.aux = g.aux; ep.ldaux = g.ldaux; ep.epilogue = g.epilogue;
+  ep.aux_evict_first = gemm_l2_hints();
   ep.nostore = gemm_debug_nostore();
   ep.tma_store = 0;
   ep.colsum = nullptr;

@@ -25,7 +25,8 @@ def apply(v, reset=False):
         return
     for kv in v.split(","):
         k, val = kv.split("=")
-        ops.set_option(getattr(L, k), 0 if reset and k != "OPT_STREAM_K" else (2 if reset else int(val)))
+        defaults = {"OPT_STREAM_K": 2, "OPT_GEMM_L2_HINTS": 1, "OPT_LN_CTAS_PER_SM": 1}
+        ops.set_option(getattr(L, k), defaults.get(k, 0) if reset else int(val))
 
 
 for _ in range(3):
