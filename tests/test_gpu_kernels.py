@@ -504,8 +504,8 @@ def test_attention_gpt10b_width():
                                        (300, 416, 128, "res"), (512, 768, 256, "dgelu")])
 def test_gemm_epilogue_warps_bitwise(M, N, K, epi):
     """4 or 8 epilogue warps (BP_OPT_GEMM_EPI_WARPS; 8 splits each TMEM lane
-    quarter's columns over two warps) and the per-thread store epilogue give
-    bit-identical outputs (C and the GELU pre-activation) for every epilogue
+    quarter's columns over two warps), with or without the L2 cache hints,
+    and the per-thread store epilogue give bit-identical outputs (C and the GELU pre-activation) for every epilogue
     kind, one or several tiles per CTA pair, ragged M and N."""
     from paper_2410_19367_b200.runtime.lib import OPT_GEMM_EPI_WARPS, OPT_GEMM_TMA_STORE
     dev = "cuda"
@@ -522,11 +522,13 @@ def test_gemm_epilogue_warps_bitwise(M, N, K, epi):
     if epi == "dgelu":
         kw["aux"] = torch.randn(M, N, device=dev).bfloat16()
         kw["epilogue"] = EPI_DGELU
+    from paper_2410_19367_b200.runtime.lib import OPT_GEMM_L2_HINTS
     outs = {}
     try:
-        for name, tma, ew in (("thread", 0, 0), ("tma4", 1, 4), ("tma8", 1, 8)):
+        for name, tma, ew, l2 in (("thread", 0, 0, 1), ("tma4", 1, 4, 1), ("tma8", 1, 8, 1), ("tma8_nohint", 1, 8, 0)):
             ops.set_option(OPT_GEMM_TMA_STORE, tma)
             ops.set_option(OPT_GEMM_EPI_WARPS, ew)
+            ops.set_option(OPT_GEMM_L2_HINTS, l2)
             C = torch.full((M, N), 7.0, device=dev, dtype=torch.bfloat16)
             if epi == "gelu":
                 kw["aux"] = torch.full((M, N), 7.0, device=dev, dtype=torch.bfloat16)
@@ -536,8 +538,9 @@ def test_gemm_epilogue_warps_bitwise(M, N, K, epi):
     finally:
         ops.set_option(OPT_GEMM_TMA_STORE, 1)
         ops.set_option(OPT_GEMM_EPI_WARPS, 0)
+        ops.set_option(OPT_GEMM_L2_HINTS, 1)
     ref = outs["thread"]
-    for name in ("tma4", "tma8"):
+    for name in ("tma4", "tma8", "tma8_nohint"):
         for i in range(2):
             if ref[i] is None:
                 continue
