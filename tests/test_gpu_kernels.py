@@ -547,3 +547,29 @@ def test_gemm_epilogue_warps_bitwise(M, N, K, epi):
             assert torch.isfinite(ref[i].float()).all()
             bad = (outs[name][i].view(torch.int16) != ref[i].view(torch.int16)).nonzero()
             assert bad.numel() == 0, (name, i, int(bad.shape[0]), bad[:4].tolist())
+
+
+@pytest.mark.parametrize("exf", [3, 4, 5, 6, 7, 8])
+def test_attn_fwd_exp_modes(exf):
+    """The forward's FMA-pipe exponential modes (BP_OPT_ATTN_FWD_EXF; measured
+    no faster than the default 2, kept as measurement options) agree with
+    the default to bf16 rounding of P (causal, S = 512, Dh = 128)."""
+    from paper_2410_19367_b200.runtime.lib import OPT_ATTN_FWD_EXF, OPT_ATTN_FWD_MODE
+    B, S, H, Dh = 1, 512, 4, 128
+    torch.manual_seed(exf)
+    qkv = torch.randn(B * S, 3 * H * Dh, device="cuda").bfloat16()
+    outs = []
+    try:
+        ops.set_option(OPT_ATTN_FWD_MODE, 1)
+        for mode in (0, exf):
+            ops.set_option(OPT_ATTN_FWD_EXF, mode)
+            o = torch.empty(B * S, H * Dh, device="cuda", dtype=torch.bfloat16)
+            lse = torch.empty(B * H * S, device="cuda")
+            ops.attn_fwd(qkv, o, lse, B, S, H, Dh, True, 1 / math.sqrt(Dh))
+            torch.cuda.synchronize()
+            outs.append((o.float(), lse))
+    finally:
+        ops.set_option(OPT_ATTN_FWD_EXF, 0)
+        ops.set_option(OPT_ATTN_FWD_MODE, 0)
+    assert _relerr(outs[1][0], outs[0][0]) < 5e-3
+    assert (outs[1][1] - outs[0][1]).abs().max().item() < 1e-3

@@ -175,20 +175,23 @@ def test_fp32_weight_gradient_placement(label, defer):
 def test_cuda_graph_replay_equals_eager(dtype):
     """A captured-and-replayed train step (Trainer.enable_graph) continues the
     eager trajectory: same per-micro-batch losses and AdamW weights after
-    three steps (device-side step counter, warm buffer pool), with new input
-    tensors copied into the captured ones."""
+    four steps (device-side step counter, warm buffer pool), with new input
+    tensors copied into the captured ones; Trainer.disable_graph returns to
+    eager launches on the same trajectory."""
     from paper_2410_19367_b200.runtime.executor import Trainer
     cfg = CONFIGS["tiny"]
     sched = ps.build_bitpipe(4, 8)
     opt = OptimConfig(lr=1e-3)
     params = init_params(cfg, 7, perturb=True)
-    batches = [synthetic_batch(cfg, sched.N, seed=20 + i) for i in range(3)]
+    batches = [synthetic_batch(cfg, sched.N, seed=20 + i) for i in range(4)]
     a = Trainer(cfg, sched, dtype=dtype, optim=opt, params=params)
     b = Trainer(cfg, sched, dtype=dtype, optim=opt, params=params)
     for i, (tok, tgt) in enumerate(batches):
         la = a.train_step(tok.int().cuda(), tgt.int().cuda()).losses.clone()
         if i == 1:
             b.enable_graph()
+        if i == 3:
+            b.disable_graph()   # back to eager launches (the bench's GEMM probe does this)
         lb = b.train_step(tok.int().cuda(), tgt.int().cuda()).losses.clone()
         torch.cuda.synchronize()
         assert rel(lb.cpu(), la.cpu()) < (1e-6 if dtype == torch.float32 else 1e-3), i
