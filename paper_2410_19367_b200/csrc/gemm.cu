@@ -8,7 +8,10 @@
 //     lane issues tcgen05.mma, tcgen05.commit frees smem slots / signals
 //     the epilogue), warp 2: TMEM allocator, warps 4-7: epilogue
 //     (tcgen05.ld 32x32b -> registers -> fused bias / GELU / dGELU /
-//     residual / fp32-accumulate -> global).
+//     residual / fp32-accumulate -> global); the CTA-pair kernel runs
+//     warps 4-11 (two per TMEM lane quarter, half the columns each) when a
+//     launch has one tile per pair and its epilogue cannot hide behind a
+//     next tile's MMAs.
 //   * A and B may each be K-major or MN-major; the smem descriptors and
 //     the instruction descriptor's transpose bits absorb the layout, so
 //     fprop (X W^T), dgrad (dY W) and wgrad (dY^T X) run without any
