@@ -47,22 +47,24 @@ __global__ void __launch_bounds__(256, 1) mma_rate(int rounds, long long* out, v
   const uint32_t tmem = slot;
   if (warp >= 4 && BG != 0) {  // background traffic until the MMA thread is done
     const int w4 = warp - 4;
+    // BG 6: all three at once (warp 4 ld, warp 5 st, warps 6-7 bulk copies), as in the forward
+    const int bg = BG != 6 ? BG : (w4 == 0 ? 1 : w4 == 1 ? 4 : 5);
     float acc = 0.f;
     uint4* region = reinterpret_cast<uint4*>(smem + 131072);  // 16 KB per warp... past the operands
     long long n = 0;
     while (*stop == 0) {
-      if (BG == 1) {
+      if (bg == 1) {
         float v[32];
         tmem_ld_32x32b_x32(tmem + ((uint32_t)(w4 * 32) << 16) + 384, v);
 #pragma unroll
         for (int i = 0; i < 32; ++i) acc += v[i];
-      } else if (BG == 4) {
+      } else if (bg == 4) {
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = acc + i;
         tmem_st_32x32b_x32(tmem + ((uint32_t)(w4 * 32) << 16) + 448, v);
         tmem_wait_st();
-      } else if (BG == 5) {
+      } else if (bg == 5) {
         // bulk async copies global -> shared, 16 KB per warp per round (TMA-like tile writes)
         if (lane == 0) {
           uint64_t* b = &bgbar[w4];
@@ -71,7 +73,7 @@ __global__ void __launch_bounds__(256, 1) mma_rate(int rounds, long long* out, v
           mbar_wait(b, n & 1);
         }
         __syncwarp();
-      } else if (BG == 2) {
+      } else if (bg == 2) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) region[(w4 * 8 + i) * 32 + lane] = make_uint4(n, i, lane, w4);
       } else {
@@ -174,6 +176,7 @@ int main() {
   run<5, 1>("attention fwd MMA sequence + tcgen05.ld loop", 148);
   run<5, 4>("attention fwd MMA sequence + tcgen05.st loop", 148);
   run<5, 5>("attention fwd MMA sequence + bulk g2s loop", 148);
+  run<5, 6>("attention fwd MMA sequence + ld + st + bulk g2s", 148);
   run<0, 5>("SS N128 + bulk g2s loop", 148);
   run<0, 1>("SS N128 + 4 warps tcgen05.ld loop", 148);
   run<1, 1>("TS N128 + 4 warps tcgen05.ld loop", 148);
