@@ -386,8 +386,7 @@ fwd_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ 
       TRACE(32 + j, 1);
       tc_fence_after();
       float s[64];
-      tmem_ld_32x32b_x32_pair(tl + st * 128 + hh * 64, tl + st * 128 + hh * 64 + 32,
-                              *reinterpret_cast<float(*)[32]>(s), *reinterpret_cast<float(*)[32]>(s + 32));
+      tmem_ld_32x32b_x64(tl + st * 128 + hh * 64, s);
       tc_fence_before();
       mbar_arrive(&s_free[st]);
       TRACE(32 + j, 2);

@@ -1,7 +1,12 @@
-import math, sys, torch
+"""One vs two query-tile forward kernels (BP_OPT_ATTN_FWD_MODE 1 / 2) on
+the GPT-1.3B / BERT-large attention shapes; BP_LIB=path times another build."""
+import math, os, sys
 sys.path.insert(0, ".")
-from paper_2410_19367_b200.runtime import ops
 from paper_2410_19367_b200.runtime import lib as L
+if os.environ.get("BP_LIB"):
+    L.LIB_PATH = os.path.abspath(os.environ["BP_LIB"])
+import torch
+from paper_2410_19367_b200.runtime import ops
 def timeit(fn, iters=30):
     for _ in range(3): fn()
     torch.cuda.synchronize()
