@@ -120,6 +120,12 @@ enum bp_option {
                                 the backward reads it) and read evict_first
                                 by the dGELU epilogue (its last use); 0:
                                 default policy                               */
+  BP_OPT_GEMM_PICK = 19,      /* 2-SM GEMM tile width: 0 (default) the wave x
+                                operand-traffic model (a GEMM running alone);
+                                1 throughput pick -- 256-wide tiles wherever
+                                N >= 256 (several streams share the GPU, so
+                                idle CTA pairs are filled by other kernels;
+                                set by the co-resident executor)             */
 };
 BP_API int bp_set_option(int option, int value);
 

@@ -12,7 +12,7 @@ namespace bp {
 
 static thread_local char g_err[1024] = "";
 static std::atomic<unsigned long long> g_launches{0};
-static std::atomic<int> g_opt_attn_exact{0}, g_opt_gemm_simt{0}, g_opt_gemm_mode{0}, g_opt_stream_k{2}, g_opt_gemm_wide{0}, g_opt_gemm_debug{0}, g_opt_gemm_tma_store{1}, g_opt_ln_unfused{0}, g_opt_ln_cps{1}, g_opt_ln_bwd_mode{0}, g_opt_attn_fwd_mode{0}, g_opt_gemm_occ{0}, g_opt_gemm_grid{0}, g_opt_gemm_bn{0}, g_opt_attn_bwd_mode{0}, g_opt_gemm_ew{0}, g_opt_attn_fwd_exf{0}, g_opt_gemm_l2{1};
+static std::atomic<int> g_opt_attn_exact{0}, g_opt_gemm_simt{0}, g_opt_gemm_mode{0}, g_opt_stream_k{2}, g_opt_gemm_wide{0}, g_opt_gemm_debug{0}, g_opt_gemm_tma_store{1}, g_opt_ln_unfused{0}, g_opt_ln_cps{1}, g_opt_ln_bwd_mode{0}, g_opt_attn_fwd_mode{0}, g_opt_gemm_occ{0}, g_opt_gemm_grid{0}, g_opt_gemm_bn{0}, g_opt_attn_bwd_mode{0}, g_opt_gemm_ew{0}, g_opt_attn_fwd_exf{0}, g_opt_gemm_l2{1}, g_opt_gemm_pick{0};
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -59,6 +59,7 @@ int attn_bwd_mode() { return g_opt_attn_bwd_mode.load(); }
 int gemm_epi_warps_mode() { return g_opt_gemm_ew.load(); }
 int attn_fwd_exf() { return g_opt_attn_fwd_exf.load(); }
 int gemm_l2_hints() { return g_opt_gemm_l2.load(); }
+int gemm_pick_mode() { return g_opt_gemm_pick.load(); }
 
 }  // namespace bp
 
@@ -112,6 +113,7 @@ int bp_set_option(int option, int value) {
       bp::g_opt_attn_fwd_exf.store(value);
       return BP_OK;
     case BP_OPT_GEMM_L2_HINTS: bp::g_opt_gemm_l2.store(value); return BP_OK;
+    case BP_OPT_GEMM_PICK: bp::g_opt_gemm_pick.store(value); return BP_OK;
     case BP_OPT_GEMM_EPI_WARPS:
       if (value != 0 && value != 4 && value != 8) {
         bp::set_error("bp_set_option: GEMM epilogue warps must be 0 (auto), 4 or 8");

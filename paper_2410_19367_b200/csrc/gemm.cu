@@ -1212,9 +1212,18 @@ static int dispatch_tc2_bn(const bp_gemm_args& g, const Epi& ep, cudaStream_t st
 int gemm_wide_mode();
 
 int gemm_force_bn();
+int gemm_pick_mode();
 
 int pick_tc2_bn(int M, int N, int pairs, bool b_mn_major) {
   if (const int f = gemm_force_bn()) return f;   // measurement aid (BP_OPT_GEMM_BN)
+  // throughput pick (BP_OPT_GEMM_PICK = 1, set by the co-resident executor):
+  // several logical devices' streams share the GPU, so CTA pairs a launch
+  // leaves idle are taken by other streams' kernels and what counts is each
+  // tile's efficiency, not the launch's wave quantisation -- 256-wide tiles
+  // move the fewest operand bytes per FLOP (BERT-large D=4 N=8: 282 k ->
+  // 311 k tok/s instead of 128-wide tiles for its N = 1024 GEMMs; GPT-1.3B
+  // unchanged)
+  if (gemm_pick_mode() == 1 && N >= 256 && M >= 256) return 256;
   static const int cand[5] = {256, 512, 224, 192, 128};
   const int tm = (M + 255) / 256;
   int best = 256;

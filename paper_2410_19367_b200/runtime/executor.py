@@ -38,6 +38,7 @@ from ..model import ModelConfig, OptimConfig, resolve_partition, stage_partition
 from ..schedule import Direction, Schedule, TaskKind, canonical_replay
 from ..schedule.analysis import WeightGradTask, replay_times
 from . import ops
+from .lib import OPT_GEMM_PICK
 from .compute import StageCompute
 from .state import GEMM_WEIGHTS, BufferPool, StageParams
 
@@ -242,6 +243,11 @@ class Trainer:
         # finish together in the drain overlap (1 = one serial stream)
         import os
         nopt = max(1, int(os.environ.get("BP_OPT_STREAMS", "1")))
+        if len(self.local_devices) > 1 and not serial_streams and os.environ.get("BP_GEMM_PICK", "") == "":
+            # several logical devices' streams share this GPU: pick GEMM tiles
+            # for per-tile efficiency (csrc/gemm.cu pick_tc2_bn, BP_OPT_GEMM_PICK;
+            # BP_GEMM_PICK=0 keeps the wave-quantisation model)
+            ops.set_option(OPT_GEMM_PICK, 1)
         self.opt_streams = [self.opt_stream] + [torch.cuda.Stream(device=self.device) for _ in range(nopt - 1)]
         # distributed: one optimizer stream per local stage -- each stage's
         # replica-pair sync (NCCL all-reduce or peer-read AdamW) must not be

@@ -14,7 +14,8 @@ __all__ = ["lib", "GemmArgs", "check", "LIB_PATH", "BP_F32", "BP_BF16", "EPI_NON
            "OPT_ATTN_EXACT", "OPT_GEMM_SIMT", "OPT_GEMM_MODE",
            "OPT_STREAM_K", "OPT_GEMM_WIDE", "OPT_GEMM_DEBUG", "OPT_GEMM_TMA_STORE", "OPT_LN_UNFUSED",
            "OPT_LN_BWD_MODE", "OPT_ATTN_FWD_MODE", "OPT_GEMM_OCC", "OPT_GEMM_GRID", "OPT_GEMM_BN", "OPT_ATTN_BWD_MODE",
-           "OPT_GEMM_EPI_WARPS", "OPT_ATTN_FWD_EXF", "OPT_GEMM_L2_HINTS", "OPT_LN_CTAS_PER_SM"]
+           "OPT_GEMM_EPI_WARPS", "OPT_ATTN_FWD_EXF", "OPT_GEMM_L2_HINTS", "OPT_LN_CTAS_PER_SM",
+           "OPT_GEMM_PICK"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "libbitpipe_b200.so")
 
@@ -23,7 +24,7 @@ EPI_NONE, EPI_GELU, EPI_DGELU = 0, 1, 2
 OPT_ATTN_EXACT, OPT_GEMM_SIMT, OPT_GEMM_MODE, OPT_STREAM_K, OPT_GEMM_WIDE = 1, 2, 3, 4, 5
 OPT_GEMM_DEBUG, OPT_GEMM_TMA_STORE, OPT_LN_UNFUSED, OPT_LN_BWD_MODE, OPT_ATTN_FWD_MODE = 6, 7, 8, 10, 11
 OPT_GEMM_OCC, OPT_GEMM_GRID, OPT_GEMM_BN, OPT_ATTN_BWD_MODE, OPT_GEMM_EPI_WARPS = 12, 13, 14, 15, 16
-OPT_ATTN_FWD_EXF, OPT_GEMM_L2_HINTS, OPT_LN_CTAS_PER_SM = 17, 18, 9
+OPT_ATTN_FWD_EXF, OPT_GEMM_L2_HINTS, OPT_LN_CTAS_PER_SM, OPT_GEMM_PICK = 17, 18, 9, 19
 ABI_VERSION = 2
 
 _vp = ctypes.c_void_p
@@ -127,7 +128,8 @@ def lib() -> ctypes.CDLL:
             for env, opt in (("BP_GEMM_OCC", OPT_GEMM_OCC), ("BP_GEMM_GRID", OPT_GEMM_GRID),
                              ("BP_GEMM_BN", OPT_GEMM_BN),
                              ("BP_ATTN_BWD_MODE", OPT_ATTN_BWD_MODE), ("BP_GEMM_EW", OPT_GEMM_EPI_WARPS),
-                             ("BP_ATTN_FWD_EXF", OPT_ATTN_FWD_EXF)):
+                             ("BP_ATTN_FWD_EXF", OPT_ATTN_FWD_EXF),
+                             ("BP_GEMM_PICK", OPT_GEMM_PICK)):
                 if os.environ.get(env, "") != "":
                     h.bp_set_option(opt, int(os.environ[env]))
             _lib = h
