@@ -320,12 +320,14 @@ class Trainer:
                                       {s: work(s) for s in range(self.S)}, budget)
 
     def _stream_priorities(self, mode) -> dict:
-        """Co-resident CUDA stream priorities (lower = more urgent).  'tail':
-        the logical devices whose lists finish last in the canonical replay
-        get the highest priority, so the pipeline drain (few streams with work
-        left) is shorter; None / 'none': all equal."""
+        """Co-resident CUDA stream priorities (lower = more urgent).  'tail'
+        (the default): the logical devices whose lists finish last in the
+        canonical replay get the highest priority, so the pipeline drain (few
+        streams with work left) is shorter -- BERT-large D=4 N=8 +1.5 %
+        (316 k vs 311-312 k tok/s, same box), GPT-1.3B within noise; 'none'
+        (argument or BP_STREAM_PRIORITY): all equal."""
         import os
-        mode = mode or os.environ.get("BP_STREAM_PRIORITY")
+        mode = mode or os.environ.get("BP_STREAM_PRIORITY") or "tail"
         if mode in (None, "", "none") or len(self.local_devices) < 2:
             return {}
         if mode != "tail":
