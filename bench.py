@@ -32,9 +32,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "GPT tokens/sec/box at D=1/2/4/8 B200 (frac of roofline); bubble fraction"
-# ncu --set full, fc1 forward GEMM 2048x8192x2048 (profiles/r2_ncu_full_summary.txt,
-# round-2 capture, mean of 3 launches): dram__bytes_read.sum + dram__bytes_write.sum per launch
-TRAFFIC_FC1_BYTES = 42.104e6 + 7.097e6
+# ncu --set full, fc1 forward GEMM 2048x8192x2048 as the co-resident step issues it
+# (bias + GELU + saved pre-activation, 256-wide pair tiles, L2 hints; tools/gemm_ncu_fc1.py,
+# profiles/r2b_ncu_fc1_summary.txt, mean of 3 launches): dram__bytes_read.sum +
+# dram__bytes_write.sum per launch
+TRAFFIC_FC1_BYTES = 42.154e6 + 20.088e6
 
 
 def parse():
@@ -454,10 +456,11 @@ def main():
                          "share_of_step": gemm_share, "fc1_fprop_avg_us": fc1_us,
                          "peak_kind": f"{peak_kind} sustained (kernel timed inside a long step)",
                          "traffic_note": "dram read+write bytes per fc1-fprop launch from ncu --set full "
-                                         "(profiles/r2_ncu_full_summary.txt); the launch's algorithmic bytes are 109 MB "
-                                         "(X 8 MiB + W 32 MiB read, GELU output + pre-activation 2 x 32 MiB "
-                                         "written): the writes are still in the 126 MB L2 when it ends and "
-                                         "X / W partly hit L2, so DRAM sees less -- no wasted re-reads"},
+                                         "(profiles/r2b_ncu_fc1_summary.txt): 42.2 MB read + 20.1 MB written; "
+                                         "the launch's algorithmic bytes are 109 MB (X 8 MiB + W 32 MiB read, "
+                                         "GELU output + pre-activation 2 x 32 MiB written): the pre-activation "
+                                         "streams to DRAM (L2 evict_first), the GELU output is still in the "
+                                         "126 MB L2 when the launch ends -- no wasted re-reads"},
             "step_roofline": {"tokens_per_s": roof_tps, "frac": value / roof_tps, "F_tok": F_tok,
                               "peak_tflops": peak_sust, "peak_kind": f"{peak_kind} sustained",
                               "beta_ideal": beta_ideal, "model_tflops": value * F_tok / 1e12},
