@@ -110,8 +110,10 @@ enum bp_option {
                                 it; 1 the dQ kernel recomputes S and dP     */
   BP_OPT_GEMM_EPI_WARPS = 16, /* 2-SM GEMM epilogue warps: 0 (default) 8 on
                                 launches with one tile per CTA pair (the
-                                epilogue is exposed there), else 4; 4 / 8
-                                force (TMA-store epilogues, no stream-K)    */
+                                epilogue is exposed there) and on every
+                                launch under BP_OPT_GEMM_PICK = 1, else 4;
+                                4 / 8 force (TMA-store epilogues, no
+                                stream-K)                                    */
   BP_OPT_ATTN_FWD_EXF = 17,   /* tcgen05 attention fwd (one query tile per
                                 CTA): exponentials per 8 computed on the FMA
                                 pipe instead of the MUFU, 2..5 (0: default) */
