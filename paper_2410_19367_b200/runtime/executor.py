@@ -29,6 +29,7 @@ Placement modes
 """
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass
 
@@ -634,6 +635,12 @@ class Trainer:
         out = {}
         torch.cuda.synchronize(dev)
         saved = {k: (c.defer_wgrad, c.combined_wgrad, c._fwd_slot, c._bwd_count) for k, c in self.compute.items()}
+        # the replay these times feed models one GPU per logical device: time
+        # each task with the single-launch GEMM tile model a dedicated GPU
+        # uses, not the co-resident throughput pick
+        coresident_pick = len(self.local_devices) > 1 and os.environ.get("BP_GEMM_PICK", "") == ""
+        if coresident_pick:
+            ops.set_option(OPT_GEMM_PICK, 0)
 
         def fb(comp, s):
             """One forward + backward of ``comp`` on ``st``: (F ms, B ms)."""
@@ -691,6 +698,8 @@ class Trainer:
             sp.grad.zero_()
         for k, c in self.compute.items():
             c.defer_wgrad, c.combined_wgrad, c._fwd_slot, c._bwd_count = saved[k]
+        if coresident_pick:
+            ops.set_option(OPT_GEMM_PICK, 1)
         return out
 
     def replay_bubble(self, times: dict, deferred_w: bool = False) -> dict:
