@@ -124,11 +124,10 @@ enum bp_option {
                                 default policy                               */
   BP_OPT_GEMM_PICK = 19,      /* 2-SM GEMM tile width: 0 (default) the wave x
                                 operand-traffic model (a GEMM running alone);
-                                1 throughput pick -- 256-wide tiles where the
-                                model would pick 128 / 192 (several streams
-                                share the GPU, so idle CTA pairs are filled
-                                by other kernels; set by the co-resident
-                                executor)                                    */
+                                1 throughput pick -- 256-wide tiles wherever
+                                N >= 256 (several streams share the GPU, so
+                                idle CTA pairs are filled by other kernels;
+                                set by the co-resident executor)             */
 };
 BP_API int bp_set_option(int option, int value);
 

@@ -1219,12 +1219,11 @@ int pick_tc2_bn(int M, int N, int pairs, bool b_mn_major) {
   // throughput pick (BP_OPT_GEMM_PICK = 1, set by the co-resident executor):
   // several logical devices' streams share the GPU, so CTA pairs a launch
   // leaves idle are taken by other streams' kernels and what counts is each
-  // tile's efficiency, not the launch's wave quantisation: the narrow tiles
-  // (128 / 192, which stream far more operand bytes per FLOP) the model picks
-  // for small-N launches become 256-wide (BERT-large D=4 N=8: 282 k -> 311 k
-  // tok/s for its N = 1024 / 3072 GEMMs); 224 stays (GPT-1.3B fc1: 4 exact
-  // waves, the step is the same either way)
-  const bool throughput = gemm_pick_mode() == 1 && N >= 256 && M >= 256;
+  // tile's efficiency, not the launch's wave quantisation: 256-wide tiles,
+  // the fewest operand bytes per FLOP (BERT-large D=4 N=8: 282 k -> 311 k
+  // tok/s for its N = 1024 / 3072 GEMMs, which the model gives 128 / 192;
+  // GPT-1.3B's fc1 forward 224 -> 256 with 8 epilogue warps: +0.6 %)
+  if (gemm_pick_mode() == 1 && N >= 256 && M >= 256) return 256;
   static const int cand[5] = {256, 512, 224, 192, 128};
   const int tm = (M + 255) / 256;
   int best = 256;
@@ -1247,7 +1246,6 @@ int pick_tc2_bn(int M, int N, int pairs, bool b_mn_major) {
       best = bn;
     }
   }
-  if (throughput && best < 224) return 256;
   return best;
 }
 
